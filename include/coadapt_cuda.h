@@ -1,0 +1,239 @@
+/*
+ * coadapt_cuda.h — C-ABI of the B200 GNS hot path (libcoadapt_b200.so).
+ *
+ * The reference (arXiv 2604.26687 artifact, proj/include/coadapt/) exposes
+ * the hot path as a C++ API whose inputs are host scalars and host spans:
+ * callers compute s_m themselves and pass it to
+ *   StepAccumulator::record_micro_batch(double)        gns.hpp:19-20
+ * and the mean-gradient norm goes through
+ *   finalize_step(acc, std::span<const double>)        gns.hpp:47-48
+ *   finalize_step(acc, double mean_grad_sq)            gns.hpp:49
+ * followed by update_ema (gns.hpp:67-68) and gns() (gns.hpp:73); the
+ * all-reduce of Algorithm 1 is "modeled as summation over the
+ * lists" (gns.hpp:11-14).  This header is the device-resident
+ * replacement a foreign-language binding (ctypes, cgo, JNI, N-API) would bind:
+ * plain pointers and sizes, no C++ or torch types, no exceptions.  Each entry
+ * point names the reference interface it replaces.
+ *
+ * Conventions
+ *  - every function returns a status: COADAPT_OK or one of the COADAPT_E_*
+ *    codes, which mirror the exception taxonomy of errors.hpp:8-27 (and the
+ *    CLI exit codes of SPEC.md:635); coadapt_last_error() returns the
+ *    thread-local message of the last failure on the calling thread.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  All device work is asynchronous on that stream; only
+ *    coadapt_gns_result / coadapt_gns_read_partials block.
+ *  - device gradient buffers are borrowed (like std::span): the library never
+ *    frees or retains them past the call's stream work.
+ *  - one coadapt_gns per (device, stream); it is not thread-safe.
+ */
+#ifndef COADAPT_CUDA_H
+#define COADAPT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COADAPT_ABI_VERSION 1
+
+/* status codes (errors.hpp:8-27) */
+#define COADAPT_OK 0
+#define COADAPT_E_VALIDATION 1 /* ValidationError: contract violated (errors.hpp:10) */
+#define COADAPT_E_INTERNAL 2   /* InternalError: library bug (errors.hpp:24) */
+#define COADAPT_E_CUDA 3       /* CUDA runtime / device failure */
+#define COADAPT_E_NCCL 4       /* NCCL failure */
+
+/* gradient element types */
+#define COADAPT_BF16 0
+#define COADAPT_FP16 1
+#define COADAPT_FP32 2
+#define COADAPT_FP64 3
+
+/* A weighted range of a rank's flattened gradient bucket, in elements.
+ * weight 0 marks a tensor that another rank already counts (a TP-replicated
+ * norm/bias on tp_rank != 0, the tied-embedding copy on the last PP stage):
+ * its bytes are never loaded.  Derived from ModelSpec.tp_split_axis = none
+ * and layout_for replication. */
+typedef struct coadapt_segment {
+  uint64_t offset;
+  uint64_t numel;
+  double weight;
+} coadapt_segment;
+
+/* Synthetic-gradient layout: bucket elements [local_off, local_off+numel)
+ * hold logical parameter indices
+ *   global_base + (j / row_len) * row_stride + (j % row_len). */
+typedef struct coadapt_gen_segment {
+  uint64_t local_off;
+  uint64_t numel;
+  uint64_t global_base;
+  uint64_t row_len;
+  uint64_t row_stride;
+} coadapt_gen_segment;
+
+/* StepStats, gns.hpp:35-40 */
+typedef struct coadapt_step_stats {
+  double signal;
+  double noise;
+  double noise_raw;
+  double mean_grad_sq;
+} coadapt_step_stats;
+
+/* GnsState, gns.hpp:53-62 (field order and defaults identical) */
+typedef struct coadapt_gns_state {
+  double ema_signal;
+  double ema_noise;
+  double alpha_early;           /* 0.95 */
+  double alpha_late;            /* 0.99 */
+  int64_t phase_boundary_tokens; /* 8'000'000 */
+  int64_t tokens_seen;
+  double calibration;           /* 2.0 */
+  int32_t initialized;
+  int32_t reserved_;
+} coadapt_gns_state;
+
+/* Everything one optimizer step produces. */
+typedef struct coadapt_gns_result {
+  coadapt_step_stats stats;  /* finalize_step, gns.hpp:47-49 */
+  coadapt_gns_state state;   /* after update_ema, gns.hpp:67-68 */
+  double phi;                /* gns(), gns.hpp:73; NaN while unavailable */
+  double b_simple;           /* this step's noise / signal (uncalibrated) */
+  int64_t sample_count;      /* N = d * M */
+  int32_t phi_available;
+  int32_t status;            /* COADAPT_OK, or COADAPT_E_VALIDATION when a
+                                partial was negative/non-finite (gns.hpp:19);
+                                the state is then left unchanged */
+} coadapt_gns_result;
+
+typedef struct coadapt_plan coadapt_plan; /* one bucket layout */
+typedef struct coadapt_gns coadapt_gns;   /* one step accumulator + GnsState */
+
+/* ---------------------------------------------------------------- misc */
+const char* coadapt_last_error(void);
+int coadapt_abi_version(void);
+/* number of kernels this library has launched in this process */
+uint64_t coadapt_kernel_launches(void);
+/* device properties the kernels size themselves by */
+int coadapt_device_info(int device, int* sm_count, int* l2_bytes,
+                        int* cc_major, int* cc_minor);
+
+/* ---------------------------------------------------------------- plan
+ * Compiles a segment table into the device range table the reductions walk.
+ * Replaces nothing in the reference directly: it is the layout half of the
+ * caller-side "Local squared norm" computation that feeds
+ * record_micro_batch (gns.hpp:19-20). */
+int coadapt_plan_create(const coadapt_segment* segs, size_t nseg,
+                        uint64_t bucket_numel, int dtype, int device,
+                        coadapt_plan** out);
+/* the same bucket restricted to DP slice `index` of `count` equal parts of
+ * its element range (the d > 1 mean-gradient read) */
+int coadapt_plan_create_slice(const coadapt_segment* segs, size_t nseg,
+                              uint64_t bucket_numel, int dtype, int device,
+                              int index, int count, coadapt_plan** out);
+int coadapt_plan_destroy(coadapt_plan* plan);
+/* elements actually loaded per pass (weight != 0) and range count */
+int coadapt_plan_info(const coadapt_plan* plan, uint64_t* active_elems,
+                      uint64_t* nranges);
+
+/* ---------------------------------------------------------------- step
+ * coadapt_gns is the device-resident StepAccumulator (gns.hpp:15-32) of one
+ * optimizer step plus a persistent GnsState (gns.hpp:53-62).  Its N+1 fp64
+ * slots hold s_{i_d,m} at i_d*M + m and gbar^2 at N.
+ * Replaces: StepAccumulator(int dp_size, int64_t global_batch) gns.hpp:17. */
+int coadapt_gns_create(int dp_size, int micro_count, int64_t global_batch,
+                       int device, coadapt_gns** out);
+int coadapt_gns_destroy(coadapt_gns* g);
+/* Scale-BS / Reconfigure: new (d, M, B_g) for the next step; keeps the EMA */
+int coadapt_gns_reshape(coadapt_gns* g, int dp_size, int micro_count,
+                        int64_t global_batch);
+/* zero the slots (start of an optimizer step) */
+int coadapt_gns_begin_step(coadapt_gns* g, void* stream);
+
+/* s_{dp_index, micro} += sum_seg w * ||bucket[seg]||^2 (fp64).
+ * Replaces: the caller's s_m computation + record_micro_batch, gns.hpp:19-20
+ * (PAPER.md:437-440).  Partials of model-parallel ranks hosted on the same
+ * device accumulate into the same slot in stream order. */
+int coadapt_gns_micro_sqnorm(coadapt_gns* g, const coadapt_plan* plan,
+                             const void* bucket, int dp_index, int micro,
+                             void* stream);
+/* `count` buckets sharing one plan in one launch */
+int coadapt_gns_micro_sqnorm_batched(coadapt_gns* g, const coadapt_plan* plan,
+                                     const void* const* buckets,
+                                     const int32_t* dp_index,
+                                     const int32_t* micro, int count,
+                                     void* stream);
+/* d == 1 fused pass over the M resident micro-buckets of this rank: every
+ * s_{0,m} and gbar^2 += ||sum_m g_m||^2 / M^2 (fp32 micro-batch sum, as
+ * Megatron's main_grad) in ONE read of the bytes.  1 <= M <= 16.
+ * Replaces: M x (s_m + record_micro_batch) and finalize_step's own
+ * ||mean_gradient||^2 (gns.hpp:45-48). */
+int coadapt_gns_fused_sqnorm(coadapt_gns* g, const coadapt_plan* plan,
+                             const void* const* buckets, int micro_count,
+                             void* stream);
+/* gbar^2 += ||mean_grad[plan]||^2 for the synchronised mean gradient
+ * (this DP replica's slice).  Replaces finalize_step's mean-gradient
+ * overload, gns.hpp:47-48. */
+int coadapt_gns_mean_sqnorm(coadapt_gns* g, const coadapt_plan* plan,
+                            const void* mean_grad, void* stream);
+/* As coadapt_gns_fused_sqnorm, but the M buckets live in HOST memory
+ * (pinned for overlap): chunks are streamed H2D through a staging ring
+ * owned by g and reduced as they land.  This is the reference-facing path
+ * for host-resident gradients (the reference's CPU call signature). */
+int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* plan,
+                                  const void* const* host_buckets,
+                                  int micro_count, void* stream);
+
+/* NCCL over NVLink: sum the N+1 slots over all ranks (Alg. 1 AllReduce,
+ * PAPER.md:443; the reference models it as summation). */
+int coadapt_nccl_unique_id(void* out, size_t len); /* len >= 128 */
+int coadapt_gns_attach_nccl(coadapt_gns* g, int nranks, int rank,
+                            const void* unique_id, size_t len);
+int coadapt_gns_allreduce(coadapt_gns* g, void* stream);
+
+/* finalize_step + update_ema + gns on the device (gns.hpp:42-73), one
+ * thread, IEEE-exact twin of the host formulas.  Copies the result to
+ * pinned host memory on `stream`.  Replaces: finalize_step(acc, double)
+ * gns.hpp:49, update_ema gns.hpp:67-68, gns gns.hpp:73. */
+int coadapt_gns_finalize(coadapt_gns* g, int64_t tokens_this_step,
+                         void* stream);
+/* waits for the last finalize and returns its result */
+int coadapt_gns_read_result(coadapt_gns* g, coadapt_gns_result* out);
+/* synchronous read of the N+1 slots (s values, then gbar^2) */
+int coadapt_gns_read_partials(coadapt_gns* g, double* out, size_t n);
+/* checkpoint / restore of the device GnsState (synchronous) */
+int coadapt_gns_get_state(coadapt_gns* g, coadapt_gns_state* out);
+int coadapt_gns_set_state(coadapt_gns* g, const coadapt_gns_state* in);
+
+/* ---------------------------------------------------------------- one-shot
+ * ||v||^2 of a device vector of `dtype` (fp64 accumulation), synchronous.
+ * Backs finalize_step(acc, std::span<const double>) (gns.hpp:47-48) when
+ * called with host data via coadapt_sqnorm_host. */
+int coadapt_sqnorm_device(const void* v, uint64_t n, int dtype, int device,
+                          double* out, void* stream);
+int coadapt_sqnorm_host(const void* v, uint64_t n, int dtype, int device,
+                        double* out);
+
+/* ---------------------------------------------------------------- synthetic
+ * Deterministic synthetic micro-gradients (device twin of the CPU oracle's
+ * integer-exact generator; test and benchmark data, K0).  Family of
+ * simulate_micro_gradients, gns.hpp:75-80. */
+int coadapt_synth_fill(void* dst, int dtype, const coadapt_gen_segment* segs,
+                       size_t nseg, uint64_t seed, uint64_t sample, float g0,
+                       float noise_unit, void* stream);
+int coadapt_synth_mean_fill(void* dst, int dtype,
+                            const coadapt_gen_segment* segs, size_t nseg,
+                            uint64_t seed, uint64_t sample0, int64_t nsamples,
+                            float g0, float noise_unit, void* stream);
+/* a streaming write of `bytes` (L2 flush between timed iterations) */
+int coadapt_l2_flush(void* scratch, uint64_t bytes, void* stream);
+/* read-only streaming peak probe: sums `bytes` of `buf` (bench roofline) */
+int coadapt_read_probe(const void* buf, uint64_t bytes, double* sink,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COADAPT_CUDA_H */

@@ -1,0 +1,865 @@
+// cabi.cu — the extern "C" boundary declared in include/coadapt_cuda.h.
+// Owns plans (device range tables), step accumulators (device slots +
+// GnsState), the NCCL communicator and the host-streaming staging ring.
+// No C++ exception crosses this boundary; failures return a status and set
+// a thread-local message (errors.hpp taxonomy, SPEC.md:635 exit codes).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/coadapt_cuda.h"
+#include "internal.h"
+
+using coadapt::dev::BatchArgs;
+using coadapt::dev::FusedArgs;
+using coadapt::dev::Range;
+using coadapt::dev::Sink;
+using coadapt::dev::Window;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+}  // namespace
+
+namespace coadapt_capi {
+// used by the C++-API bindings (host/capi.cpp) to share the message slot
+void set_error(const char* msg) { g_err = msg ? msg : ""; }
+}  // namespace coadapt_capi
+
+namespace {
+
+#define CU(call)                                                          \
+  do {                                                                    \
+    cudaError_t e_ = (call);                                              \
+    if (e_ != cudaSuccess)                                                \
+      return fail(COADAPT_E_CUDA, std::string(#call) + ": " +             \
+                                      cudaGetErrorString(e_));            \
+  } while (0)
+
+#define NC(call)                                                          \
+  do {                                                                    \
+    ncclResult_t r_ = (call);                                             \
+    if (r_ != ncclSuccess)                                                \
+      return fail(COADAPT_E_NCCL,                                         \
+                  std::string(#call) + ": " + ncclGetErrorString(r_));    \
+  } while (0)
+
+// Makes `dev` current for the scope of a call and restores the caller's.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev)
+      cudaSetDevice(prev);
+  }
+};
+
+#define GUARD(dev)                                                        \
+  DeviceGuard guard_(dev);                                                \
+  if (guard_.err != cudaSuccess)                                          \
+    return fail(COADAPT_E_CUDA, std::string("device ") +                  \
+                                    std::to_string(dev) + ": " +          \
+                                    cudaGetErrorString(guard_.err))
+
+int esize(int dtype) {
+  switch (dtype) {
+    case COADAPT_BF16:
+    case COADAPT_FP16: return 2;
+    case COADAPT_FP32: return 4;
+    case COADAPT_FP64: return 8;
+  }
+  return 0;
+}
+
+int sm_count(int dev) {
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
+      cudaSuccess)
+    return 0;
+  return n;
+}
+
+// CTAs for a reduction over `active` elements: a full resident wave
+// (SMs x occupancy) unless the pass is too small to feed it (>= 16 Ki
+// elements per CTA keeps the per-CTA fixed cost below a few percent).
+int grid_for(int dev, int occ, uint64_t active) {
+  const int full = std::max(1, sm_count(dev) * std::max(1, occ));
+  const uint64_t by_size = (active + 16383) / 16384;
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(full, by_size));
+}
+
+constexpr int kMaxGridPerSM = 8;  // 2048 threads / 256
+constexpr uint64_t kStageElems = 16ull << 20;  // host streaming chunk
+constexpr int kStages = 3;
+
+}  // namespace
+
+struct coadapt_plan {
+  int device = 0;
+  int dtype = COADAPT_BF16;
+  uint64_t bucket_numel = 0;
+  uint64_t active = 0;
+  std::vector<Range> host;  // ranges, sorted, merged
+  Range* ranges = nullptr;  // device copy
+};
+
+struct coadapt_gns {
+  int device = 0;
+  int dp = 1, M = 1, N = 1;
+  int64_t global_batch = 0;
+  int sms = 0;
+  double* slots = nullptr;      // N+1 (capacity slot_cap)
+  int slot_cap = 0;
+  double* partials = nullptr;   // per-CTA partials
+  size_t partial_cap = 0;       // doubles
+  unsigned int* ticket = nullptr;
+  void* state = nullptr;        // coadapt_gns_state (device)
+  void* result = nullptr;       // coadapt_gns_result (device)
+  coadapt_gns_result* result_host = nullptr;  // pinned
+  cudaEvent_t result_ready = nullptr;
+  bool finalized = false;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  // host streaming (coadapt_gns_fused_sqnorm_host)
+  void* staging = nullptr;  // kStages * 16 * kStageElems * es bytes
+  size_t staging_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t stage_free[kStages] = {};
+  cudaEvent_t stage_full[kStages] = {};
+};
+
+namespace {
+
+int alloc_slots(coadapt_gns* g, int n_slots) {
+  if (n_slots <= g->slot_cap) return COADAPT_OK;
+  if (g->slots) cudaFree(g->slots);
+  g->slots = nullptr;
+  CU(cudaMalloc(&g->slots, sizeof(double) * n_slots));
+  CU(cudaMemset(g->slots, 0, sizeof(double) * n_slots));
+  g->slot_cap = n_slots;
+  return COADAPT_OK;
+}
+
+int validate_dtype(int dtype, bool fp64_ok) {
+  if (dtype == COADAPT_BF16 || dtype == COADAPT_FP16 ||
+      dtype == COADAPT_FP32 || (fp64_ok && dtype == COADAPT_FP64))
+    return COADAPT_OK;
+  return fail(COADAPT_E_VALIDATION, "unsupported dtype " + std::to_string(dtype));
+}
+
+int build_ranges(const coadapt_segment* segs, size_t nseg,
+                 uint64_t bucket_numel, uint64_t lo, uint64_t hi,
+                 std::vector<Range>& out, uint64_t& active) {
+  std::vector<coadapt_segment> v(segs, segs + nseg);
+  for (const auto& s : v) {
+    if (!std::isfinite(s.weight))
+      return fail(COADAPT_E_VALIDATION, "segment weight is not finite");
+    if (s.offset > bucket_numel || s.numel > bucket_numel - s.offset)
+      return fail(COADAPT_E_VALIDATION,
+                  "segment [" + std::to_string(s.offset) + ", +" +
+                      std::to_string(s.numel) + ") exceeds bucket of " +
+                      std::to_string(bucket_numel) + " elements");
+  }
+  std::stable_sort(v.begin(), v.end(),
+                   [](const coadapt_segment& a, const coadapt_segment& b) {
+                     return a.offset < b.offset;
+                   });
+  for (size_t i = 1; i < v.size(); ++i)
+    if (v[i].offset < v[i - 1].offset + v[i - 1].numel)
+      return fail(COADAPT_E_VALIDATION, "segments overlap at element " +
+                                            std::to_string(v[i].offset));
+  out.clear();
+  active = 0;
+  for (const auto& s : v) {
+    if (s.weight == 0.0 || s.numel == 0) continue;
+    uint64_t b = std::max(s.offset, lo), e = std::min(s.offset + s.numel, hi);
+    if (b >= e) continue;
+    if (!out.empty() && out.back().weight == s.weight &&
+        out.back().abs_begin + out.back().len == b) {
+      out.back().len += e - b;
+    } else {
+      out.push_back(Range{b, active, e - b, s.weight});
+    }
+    active += e - b;
+  }
+  return COADAPT_OK;
+}
+
+int plan_make(const coadapt_segment* segs, size_t nseg, uint64_t bucket_numel,
+              int dtype, int device, uint64_t lo, uint64_t hi,
+              coadapt_plan** out) {
+  if (!out) return fail(COADAPT_E_VALIDATION, "out is NULL");
+  *out = nullptr;
+  if (nseg && !segs) return fail(COADAPT_E_VALIDATION, "segs is NULL");
+  if (int rc = validate_dtype(dtype, true)) return rc;
+  GUARD(device);
+  auto* p = new coadapt_plan;
+  p->device = device;
+  p->dtype = dtype;
+  p->bucket_numel = bucket_numel;
+  if (int rc = build_ranges(segs, nseg, bucket_numel, lo, hi, p->host,
+                            p->active)) {
+    delete p;
+    return rc;
+  }
+  if (!p->host.empty()) {
+    cudaError_t e = cudaMalloc(&p->ranges, sizeof(Range) * p->host.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->ranges, p->host.data(), sizeof(Range) * p->host.size(),
+                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      if (p->ranges) cudaFree(p->ranges);
+      delete p;
+      return fail(COADAPT_E_CUDA, std::string("plan upload: ") +
+                                      cudaGetErrorString(e));
+    }
+  }
+  *out = p;
+  return COADAPT_OK;
+}
+
+int check_bucket(const coadapt_plan* p, const void* ptr, const char* what) {
+  if (!ptr && p->active) return fail(COADAPT_E_VALIDATION, std::string(what) + " is NULL");
+  if (reinterpret_cast<uintptr_t>(ptr) % esize(p->dtype))
+    return fail(COADAPT_E_VALIDATION,
+                std::string(what) + " is not aligned to its element size");
+  return COADAPT_OK;
+}
+
+int ensure_partials(coadapt_gns* g, size_t n) {
+  if (n <= g->partial_cap) return COADAPT_OK;
+  // growth is a synchronous cudaFree/cudaMalloc: callers size it up front
+  if (g->partials) {
+    CU(cudaDeviceSynchronize());
+    cudaFree(g->partials);
+    g->partials = nullptr;
+  }
+  CU(cudaMalloc(&g->partials, n * sizeof(double)));
+  g->partial_cap = n;
+  return COADAPT_OK;
+}
+
+int check_slot(const coadapt_gns* g, int dp_index, int micro) {
+  if (dp_index < 0 || dp_index >= g->dp || micro < 0 || micro >= g->M)
+    return fail(COADAPT_E_VALIDATION,
+                "slot (dp=" + std::to_string(dp_index) + ", m=" +
+                    std::to_string(micro) + ") outside d=" +
+                    std::to_string(g->dp) + ", M=" + std::to_string(g->M));
+  return COADAPT_OK;
+}
+
+int launch_batch(coadapt_gns* g, const coadapt_plan* p, const BatchArgs& jobs,
+                 Window w, cudaStream_t s) {
+  const uint64_t n = w.e_end - w.e_begin;
+  if (n == 0 || jobs.count == 0) return COADAPT_OK;
+  const int grid =
+      grid_for(g->device, coadapt::dev::occupancy_sqnorm(p->dtype), n);
+  if (int rc = ensure_partials(g, (size_t)grid * jobs.count)) return rc;
+  Sink sink{g->partials, g->ticket, g->slots};
+  CU(coadapt::dev::launch_sqnorm_batched(p->dtype, p->ranges,
+                                         (int)p->host.size(), w, jobs, sink,
+                                         grid, s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return COADAPT_OK;
+}
+
+int launch_fused_window(coadapt_gns* g, const coadapt_plan* p,
+                        const FusedArgs& fa, int M, Window w, cudaStream_t s) {
+  const uint64_t n = w.e_end - w.e_begin;
+  if (n == 0) return COADAPT_OK;
+  const int grid =
+      grid_for(g->device, coadapt::dev::occupancy_fused(p->dtype, M), n);
+  if (int rc = ensure_partials(g, (size_t)grid * (M + 1))) return rc;
+  Sink sink{g->partials, g->ticket, g->slots};
+  CU(coadapt::dev::launch_fused(p->dtype, M, p->ranges, (int)p->host.size(), w,
+                                fa, sink, grid, s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return COADAPT_OK;
+}
+
+// compacted index of the first active element at or after abs index x
+uint64_t cum_at(const coadapt_plan* p, uint64_t x) {
+  const auto& R = p->host;
+  auto it = std::upper_bound(R.begin(), R.end(), x,
+                             [](uint64_t v, const Range& r) {
+                               return v < r.abs_begin;
+                             });
+  if (it == R.begin()) return 0;
+  --it;
+  if (x >= it->abs_begin + it->len) return it->cum_begin + it->len;
+  return it->cum_begin + (x - it->abs_begin);
+}
+
+coadapt_gns_state default_state() {
+  coadapt_gns_state s;
+  std::memset(&s, 0, sizeof(s));
+  s.alpha_early = 0.95;
+  s.alpha_late = 0.99;
+  s.phase_boundary_tokens = 8000000;
+  s.calibration = 2.0;
+  return s;
+}
+
+std::mutex g_oneshot_mu;
+
+}  // namespace
+
+// ====================================================================== API
+
+extern "C" {
+
+const char* coadapt_last_error(void) { return g_err.c_str(); }
+int coadapt_abi_version(void) { return COADAPT_ABI_VERSION; }
+uint64_t coadapt_kernel_launches(void) {
+  return g_launches.load(std::memory_order_relaxed);
+}
+
+int coadapt_device_info(int device, int* sm, int* l2, int* major, int* minor) {
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (sm) *sm = prop.multiProcessorCount;
+  if (l2) *l2 = prop.l2CacheSize;
+  if (major) *major = prop.major;
+  if (minor) *minor = prop.minor;
+  return COADAPT_OK;
+}
+
+int coadapt_plan_create(const coadapt_segment* segs, size_t nseg,
+                        uint64_t bucket_numel, int dtype, int device,
+                        coadapt_plan** out) {
+  return plan_make(segs, nseg, bucket_numel, dtype, device, 0, bucket_numel,
+                   out);
+}
+
+int coadapt_plan_create_slice(const coadapt_segment* segs, size_t nseg,
+                              uint64_t bucket_numel, int dtype, int device,
+                              int index, int count, coadapt_plan** out) {
+  if (count < 1 || index < 0 || index >= count)
+    return fail(COADAPT_E_VALIDATION, "slice index/count out of range");
+  auto cut = [&](int i) -> uint64_t {
+    if (i >= count) return bucket_numel;
+    const unsigned __int128 x = (unsigned __int128)bucket_numel * i / count;
+    return (uint64_t)x & ~uint64_t(63);
+  };
+  return plan_make(segs, nseg, bucket_numel, dtype, device, cut(index),
+                   cut(index + 1), out);
+}
+
+int coadapt_plan_destroy(coadapt_plan* p) {
+  if (!p) return COADAPT_OK;
+  {
+    DeviceGuard guard(p->device);
+    if (p->ranges) cudaFree(p->ranges);
+  }
+  delete p;
+  return COADAPT_OK;
+}
+
+int coadapt_plan_info(const coadapt_plan* p, uint64_t* active,
+                      uint64_t* nranges) {
+  if (!p) return fail(COADAPT_E_VALIDATION, "plan is NULL");
+  if (active) *active = p->active;
+  if (nranges) *nranges = p->host.size();
+  return COADAPT_OK;
+}
+
+int coadapt_gns_create(int dp_size, int micro_count, int64_t global_batch,
+                       int device, coadapt_gns** out) {
+  if (!out) return fail(COADAPT_E_VALIDATION, "out is NULL");
+  *out = nullptr;
+  if (dp_size < 1 || micro_count < 1)
+    return fail(COADAPT_E_VALIDATION, "dp_size and micro_count must be >= 1");
+  if ((int64_t)dp_size * micro_count < 2)
+    return fail(COADAPT_E_VALIDATION,
+                "N = d*M must be >= 2 (gns.hpp:45, SPEC.md:179)");
+  if (global_batch < 1)
+    return fail(COADAPT_E_VALIDATION, "global_batch must be >= 1");
+  GUARD(device);
+  auto* g = new coadapt_gns;
+  g->device = device;
+  g->dp = dp_size;
+  g->M = micro_count;
+  g->N = dp_size * micro_count;
+  g->global_batch = global_batch;
+  g->sms = sm_count(device);
+  auto cleanup = [&](int rc) {
+    coadapt_gns_destroy(g);
+    return rc;
+  };
+  if (int rc = alloc_slots(g, g->N + 1)) return cleanup(rc);
+  const size_t cap = (size_t)std::max(1, g->sms) * kMaxGridPerSM *
+                     std::max(coadapt::dev::kMaxBatch,
+                              coadapt::dev::kMaxFusedM + 1);
+  if (int rc = ensure_partials(g, cap)) return cleanup(rc);
+  cudaError_t e = cudaMalloc(&g->ticket, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(g->ticket, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&g->state, sizeof(coadapt_gns_state));
+  if (e == cudaSuccess) {
+    const coadapt_gns_state s = default_state();
+    e = cudaMemcpy(g->state, &s, sizeof(s), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&g->result, sizeof(coadapt_gns_result));
+  if (e == cudaSuccess)
+    e = cudaHostAlloc((void**)&g->result_host, sizeof(coadapt_gns_result),
+                      cudaHostAllocDefault);
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&g->result_ready, cudaEventDisableTiming);
+  if (e != cudaSuccess)
+    return cleanup(fail(COADAPT_E_CUDA, std::string("gns_create: ") +
+                                            cudaGetErrorString(e)));
+  *out = g;
+  return COADAPT_OK;
+}
+
+int coadapt_gns_destroy(coadapt_gns* g) {
+  if (!g) return COADAPT_OK;
+  {
+    DeviceGuard guard(g->device);
+    cudaDeviceSynchronize();
+    if (g->comm) ncclCommDestroy(g->comm);
+    if (g->slots) cudaFree(g->slots);
+    if (g->partials) cudaFree(g->partials);
+    if (g->ticket) cudaFree(g->ticket);
+    if (g->state) cudaFree(g->state);
+    if (g->result) cudaFree(g->result);
+    if (g->result_host) cudaFreeHost(g->result_host);
+    if (g->result_ready) cudaEventDestroy(g->result_ready);
+    if (g->staging) cudaFree(g->staging);
+    if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
+    for (int i = 0; i < kStages; ++i) {
+      if (g->stage_free[i]) cudaEventDestroy(g->stage_free[i]);
+      if (g->stage_full[i]) cudaEventDestroy(g->stage_full[i]);
+    }
+  }
+  delete g;
+  return COADAPT_OK;
+}
+
+int coadapt_gns_reshape(coadapt_gns* g, int dp_size, int micro_count,
+                        int64_t global_batch) {
+  if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
+  if (dp_size < 1 || micro_count < 1 || (int64_t)dp_size * micro_count < 2 ||
+      global_batch < 1)
+    return fail(COADAPT_E_VALIDATION, "reshape: need d, M >= 1, d*M >= 2");
+  GUARD(g->device);
+  CU(cudaDeviceSynchronize());
+  if (int rc = alloc_slots(g, dp_size * micro_count + 1)) return rc;
+  g->dp = dp_size;
+  g->M = micro_count;
+  g->N = dp_size * micro_count;
+  g->global_batch = global_batch;
+  return COADAPT_OK;
+}
+
+int coadapt_gns_begin_step(coadapt_gns* g, void* stream) {
+  if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
+  GUARD(g->device);
+  CU(cudaMemsetAsync(g->slots, 0, sizeof(double) * (g->N + 1),
+                     static_cast<cudaStream_t>(stream)));
+  return COADAPT_OK;
+}
+
+int coadapt_gns_micro_sqnorm(coadapt_gns* g, const coadapt_plan* p,
+                             const void* bucket, int dp_index, int micro,
+                             void* stream) {
+  const int32_t d = dp_index, m = micro;
+  return coadapt_gns_micro_sqnorm_batched(g, p, &bucket, &d, &m, 1, stream);
+}
+
+int coadapt_gns_micro_sqnorm_batched(coadapt_gns* g, const coadapt_plan* p,
+                                     const void* const* buckets,
+                                     const int32_t* dp_index,
+                                     const int32_t* micro, int count,
+                                     void* stream) {
+  if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
+  if (p->device != g->device)
+    return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
+  if (p->dtype == COADAPT_FP64)
+    return fail(COADAPT_E_VALIDATION, "fp64 buckets: use coadapt_sqnorm_device");
+  if (count < 0 || (count && (!buckets || !dp_index || !micro)))
+    return fail(COADAPT_E_VALIDATION, "bad batch arguments");
+  GUARD(g->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int base = 0; base < count; base += coadapt::dev::kMaxBatch) {
+    BatchArgs jobs;
+    std::memset(&jobs, 0, sizeof(jobs));
+    jobs.count = std::min(coadapt::dev::kMaxBatch, count - base);
+    for (int j = 0; j < jobs.count; ++j) {
+      if (int rc = check_slot(g, dp_index[base + j], micro[base + j])) return rc;
+      if (int rc = check_bucket(p, buckets[base + j], "bucket")) return rc;
+      jobs.ptr[j] = buckets[base + j];
+      jobs.slot[j] = dp_index[base + j] * g->M + micro[base + j];
+    }
+    if (int rc = launch_batch(g, p, jobs, Window{0, p->active}, s)) return rc;
+  }
+  return COADAPT_OK;
+}
+
+int coadapt_gns_fused_sqnorm(coadapt_gns* g, const coadapt_plan* p,
+                             const void* const* buckets, int micro_count,
+                             void* stream) {
+  if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
+  if (p->device != g->device)
+    return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
+  if (g->dp != 1)
+    return fail(COADAPT_E_VALIDATION,
+                "fused pass needs d == 1 (gbar is the local micro-batch "
+                "mean); use micro_sqnorm + mean_sqnorm for d > 1");
+  if (micro_count != g->M || micro_count < 1 ||
+      micro_count > coadapt::dev::kMaxFusedM)
+    return fail(COADAPT_E_VALIDATION,
+                "fused pass needs micro_count == M <= 16");
+  if (p->dtype == COADAPT_FP64)
+    return fail(COADAPT_E_VALIDATION, "fp64 buckets are not supported here");
+  if (!buckets) return fail(COADAPT_E_VALIDATION, "buckets is NULL");
+  FusedArgs fa;
+  std::memset(&fa, 0, sizeof(fa));
+  const uintptr_t mod0 = reinterpret_cast<uintptr_t>(buckets[0]) & 15;
+  for (int m = 0; m < micro_count; ++m) {
+    if (int rc = check_bucket(p, buckets[m], "bucket")) return rc;
+    if ((reinterpret_cast<uintptr_t>(buckets[m]) & 15) != mod0)
+      return fail(COADAPT_E_VALIDATION,
+                  "fused buckets must share their address mod 16");
+    fa.ptr[m] = buckets[m];
+  }
+  fa.slot0 = 0;
+  fa.gslot = g->N;
+  fa.gscale = 1.0 / ((double)micro_count * (double)micro_count);
+  GUARD(g->device);
+  return launch_fused_window(g, p, fa, micro_count, Window{0, p->active},
+                             static_cast<cudaStream_t>(stream));
+}
+
+int coadapt_gns_mean_sqnorm(coadapt_gns* g, const coadapt_plan* p,
+                            const void* mean_grad, void* stream) {
+  if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
+  if (p->device != g->device)
+    return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
+  if (p->dtype == COADAPT_FP64)
+    return fail(COADAPT_E_VALIDATION, "fp64: use coadapt_sqnorm_device");
+  if (int rc = check_bucket(p, mean_grad, "mean_grad")) return rc;
+  GUARD(g->device);
+  BatchArgs jobs;
+  std::memset(&jobs, 0, sizeof(jobs));
+  jobs.count = 1;
+  jobs.ptr[0] = mean_grad;
+  jobs.slot[0] = g->N;
+  return launch_batch(g, p, jobs, Window{0, p->active},
+                      static_cast<cudaStream_t>(stream));
+}
+
+int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
+                                  const void* const* host_buckets,
+                                  int micro_count, void* stream) {
+  if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
+  if (p->device != g->device)
+    return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
+  if (g->dp != 1 || micro_count != g->M || micro_count < 1 ||
+      micro_count > coadapt::dev::kMaxFusedM)
+    return fail(COADAPT_E_VALIDATION,
+                "host fused pass needs d == 1 and micro_count == M <= 16");
+  if (p->dtype == COADAPT_FP64)
+    return fail(COADAPT_E_VALIDATION, "fp64 buckets are not supported here");
+  if (!host_buckets) return fail(COADAPT_E_VALIDATION, "host_buckets is NULL");
+  for (int m = 0; m < micro_count; ++m)
+    if (!host_buckets[m] && p->active)
+      return fail(COADAPT_E_VALIDATION, "host bucket is NULL");
+  GUARD(g->device);
+  const int es = esize(p->dtype);
+  const size_t stage_stride = kStageElems * es;  // per bucket per stage
+  const size_t need = (size_t)kStages * coadapt::dev::kMaxFusedM * stage_stride;
+  if (!g->staging) {
+    CU(cudaMalloc(&g->staging, need));
+    g->staging_bytes = need;
+    CU(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < kStages; ++i) {
+      CU(cudaEventCreateWithFlags(&g->stage_free[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&g->stage_full[i], cudaEventDisableTiming));
+    }
+  } else if (g->staging_bytes < need) {
+    return fail(COADAPT_E_INTERNAL, "staging ring smaller than required");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // the compute stream must be done with every stage before we overwrite it
+  for (int i = 0; i < kStages; ++i) CU(cudaEventRecord(g->stage_free[i], s));
+  const uint64_t numel = p->bucket_numel;
+  const uint64_t nchunks = (numel + kStageElems - 1) / kStageElems;
+  for (uint64_t c = 0; c < nchunks; ++c) {
+    const uint64_t w0 = c * kStageElems;
+    const uint64_t w1 = std::min(numel, w0 + kStageElems);
+    const Window win{cum_at(p, w0), cum_at(p, w1)};
+    if (win.e_end == win.e_begin) continue;  // chunk holds only weight-0 data
+    const int st = (int)(c % kStages);
+    char* stage = static_cast<char*>(g->staging) +
+                  (size_t)st * coadapt::dev::kMaxFusedM * stage_stride;
+    CU(cudaStreamWaitEvent(g->copy_stream, g->stage_free[st], 0));
+    FusedArgs fa;
+    std::memset(&fa, 0, sizeof(fa));
+    for (int m = 0; m < micro_count; ++m) {
+      char* dst = stage + (size_t)m * stage_stride;
+      CU(cudaMemcpyAsync(dst,
+                         static_cast<const char*>(host_buckets[m]) + w0 * es,
+                         (w1 - w0) * es, cudaMemcpyHostToDevice,
+                         g->copy_stream));
+      // virtual base: abs element x of the window lives at dst + (x-w0)*es
+      fa.ptr[m] = dst - w0 * es;
+    }
+    CU(cudaEventRecord(g->stage_full[st], g->copy_stream));
+    CU(cudaStreamWaitEvent(s, g->stage_full[st], 0));
+    fa.slot0 = 0;
+    fa.gslot = g->N;
+    fa.gscale = 1.0 / ((double)micro_count * (double)micro_count);
+    if (int rc = launch_fused_window(g, p, fa, micro_count, win, s)) return rc;
+    CU(cudaEventRecord(g->stage_free[st], s));
+  }
+  return COADAPT_OK;
+}
+
+int coadapt_nccl_unique_id(void* out, size_t len) {
+  if (!out || len < sizeof(ncclUniqueId))
+    return fail(COADAPT_E_VALIDATION, "unique id buffer must be >= 128 bytes");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return COADAPT_OK;
+}
+
+int coadapt_gns_attach_nccl(coadapt_gns* g, int nranks, int rank,
+                            const void* unique_id, size_t len) {
+  if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
+  if (!unique_id || len < sizeof(ncclUniqueId))
+    return fail(COADAPT_E_VALIDATION, "unique id must be >= 128 bytes");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(COADAPT_E_VALIDATION, "bad nranks/rank");
+  GUARD(g->device);
+  if (g->comm) {
+    ncclCommDestroy(g->comm);
+    g->comm = nullptr;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  NC(ncclCommInitRank(&g->comm, nranks, id, rank));
+  g->nranks = nranks;
+  g->rank = rank;
+  return COADAPT_OK;
+}
+
+int coadapt_gns_allreduce(coadapt_gns* g, void* stream) {
+  if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
+  if (!g->comm || g->nranks == 1) return COADAPT_OK;  // local sum only
+  GUARD(g->device);
+  NC(ncclAllReduce(g->slots, g->slots, (size_t)g->N + 1, ncclFloat64, ncclSum,
+                   g->comm, static_cast<cudaStream_t>(stream)));
+  return COADAPT_OK;
+}
+
+int coadapt_gns_finalize(coadapt_gns* g, int64_t tokens, void* stream) {
+  if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
+  if (tokens < 0) return fail(COADAPT_E_VALIDATION, "tokens must be >= 0");
+  GUARD(g->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  coadapt::dev::FinalizeArgs a{g->slots, g->N, g->global_batch, tokens,
+                               g->state, g->result};
+  CU(coadapt::dev::launch_finalize(a, s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CU(cudaMemcpyAsync(g->result_host, g->result, sizeof(coadapt_gns_result),
+                     cudaMemcpyDeviceToHost, s));
+  CU(cudaEventRecord(g->result_ready, s));
+  g->finalized = true;
+  return COADAPT_OK;
+}
+
+int coadapt_gns_read_result(coadapt_gns* g, coadapt_gns_result* out) {
+  if (!g || !out) return fail(COADAPT_E_VALIDATION, "gns/out is NULL");
+  if (!g->finalized)
+    return fail(COADAPT_E_VALIDATION, "no finalized step to read");
+  GUARD(g->device);
+  CU(cudaEventSynchronize(g->result_ready));
+  *out = *g->result_host;
+  if (out->status != COADAPT_OK)
+    return fail(COADAPT_E_VALIDATION,
+                "a squared-norm partial was negative or non-finite "
+                "(gns.hpp:19); GnsState left unchanged");
+  return COADAPT_OK;
+}
+
+int coadapt_gns_read_partials(coadapt_gns* g, double* out, size_t n) {
+  if (!g || !out) return fail(COADAPT_E_VALIDATION, "gns/out is NULL");
+  if (n < (size_t)g->N + 1)
+    return fail(COADAPT_E_VALIDATION, "need N+1 doubles");
+  GUARD(g->device);
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(out, g->slots, sizeof(double) * (g->N + 1),
+                cudaMemcpyDeviceToHost));
+  return COADAPT_OK;
+}
+
+int coadapt_gns_get_state(coadapt_gns* g, coadapt_gns_state* out) {
+  if (!g || !out) return fail(COADAPT_E_VALIDATION, "gns/out is NULL");
+  GUARD(g->device);
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(out, g->state, sizeof(*out), cudaMemcpyDeviceToHost));
+  return COADAPT_OK;
+}
+
+int coadapt_gns_set_state(coadapt_gns* g, const coadapt_gns_state* in) {
+  if (!g || !in) return fail(COADAPT_E_VALIDATION, "gns/in is NULL");
+  if (!(in->alpha_early > 0.0 && in->alpha_early <= in->alpha_late &&
+        in->alpha_late < 1.0))
+    return fail(COADAPT_E_VALIDATION,
+                "need 0 < alpha_early <= alpha_late < 1 (SPEC.md:160)");
+  GUARD(g->device);
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(g->state, in, sizeof(*in), cudaMemcpyHostToDevice));
+  return COADAPT_OK;
+}
+
+int coadapt_sqnorm_device(const void* v, uint64_t n, int dtype, int device,
+                          double* out, void* stream) {
+  if (!out) return fail(COADAPT_E_VALIDATION, "out is NULL");
+  if (int rc = validate_dtype(dtype, true)) return rc;
+  std::lock_guard<std::mutex> lock(g_oneshot_mu);
+  GUARD(device);
+  coadapt_segment seg{0, n, 1.0};
+  coadapt_plan* p = nullptr;
+  if (int rc = plan_make(&seg, 1, n, dtype, device, 0, n, &p)) return rc;
+  int rc = check_bucket(p, v, "vector");
+  coadapt_gns g;  // a throwaway accumulator: one slot
+  g.device = device;
+  g.sms = sm_count(device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!rc) rc = alloc_slots(&g, 1);
+  if (!rc && cudaMalloc(&g.ticket, sizeof(unsigned int)) != cudaSuccess)
+    rc = fail(COADAPT_E_CUDA, "ticket alloc");
+  if (!rc && cudaMemsetAsync(g.ticket, 0, sizeof(unsigned int), s) != cudaSuccess)
+    rc = fail(COADAPT_E_CUDA, "ticket init");
+  if (!rc && cudaMemsetAsync(g.slots, 0, sizeof(double), s) != cudaSuccess)
+    rc = fail(COADAPT_E_CUDA, "slot init");
+  if (!rc) {
+    BatchArgs jobs;
+    std::memset(&jobs, 0, sizeof(jobs));
+    jobs.count = 1;
+    jobs.ptr[0] = v;
+    jobs.slot[0] = 0;
+    rc = launch_batch(&g, p, jobs, Window{0, p->active}, s);
+  }
+  if (!rc) {
+    cudaError_t e = cudaMemcpyAsync(out, g.slots, sizeof(double),
+                                    cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess)
+      rc = fail(COADAPT_E_CUDA, std::string("sqnorm: ") + cudaGetErrorString(e));
+  }
+  if (g.slots) cudaFree(g.slots);
+  if (g.partials) cudaFree(g.partials);
+  if (g.ticket) cudaFree(g.ticket);
+  g.slots = nullptr;
+  g.partials = nullptr;
+  g.ticket = nullptr;
+  coadapt_plan_destroy(p);
+  return rc;
+}
+
+int coadapt_sqnorm_host(const void* v, uint64_t n, int dtype, int device,
+                        double* out) {
+  if (!out) return fail(COADAPT_E_VALIDATION, "out is NULL");
+  if (int rc = validate_dtype(dtype, true)) return rc;
+  if (n == 0) {
+    *out = 0.0;
+    return COADAPT_OK;
+  }
+  if (!v) return fail(COADAPT_E_VALIDATION, "vector is NULL");
+  GUARD(device);
+  void* d = nullptr;
+  const size_t bytes = (size_t)n * esize(dtype);
+  CU(cudaMalloc(&d, bytes));
+  cudaError_t e = cudaMemcpy(d, v, bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return fail(COADAPT_E_CUDA, std::string("sqnorm_host copy: ") +
+                                    cudaGetErrorString(e));
+  }
+  const int rc = coadapt_sqnorm_device(d, n, dtype, device, out, nullptr);
+  cudaFree(d);
+  return rc;
+}
+
+int coadapt_synth_fill(void* dst, int dtype, const coadapt_gen_segment* segs,
+                       size_t nseg, uint64_t seed, uint64_t sample, float g0,
+                       float unit, void* stream) {
+  if (int rc = validate_dtype(dtype, true)) return rc;
+  if (nseg && (!segs || !dst)) return fail(COADAPT_E_VALIDATION, "NULL argument");
+  for (size_t i = 0; i < nseg; ++i) {
+    if (segs[i].row_len == 0 && segs[i].numel)
+      return fail(COADAPT_E_VALIDATION, "gen segment row_len is 0");
+    coadapt::dev::GenSeg gs{segs[i].local_off, segs[i].numel,
+                            segs[i].global_base, segs[i].row_len,
+                            segs[i].row_stride};
+    CU(coadapt::dev::launch_synth(dst, dtype, gs, seed, sample, g0, unit,
+                                  static_cast<cudaStream_t>(stream)));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  return COADAPT_OK;
+}
+
+int coadapt_synth_mean_fill(void* dst, int dtype,
+                            const coadapt_gen_segment* segs, size_t nseg,
+                            uint64_t seed, uint64_t sample0, int64_t nsamples,
+                            float g0, float unit, void* stream) {
+  if (int rc = validate_dtype(dtype, true)) return rc;
+  if (nsamples < 1) return fail(COADAPT_E_VALIDATION, "nsamples must be >= 1");
+  if (nseg && (!segs || !dst)) return fail(COADAPT_E_VALIDATION, "NULL argument");
+  for (size_t i = 0; i < nseg; ++i) {
+    if (segs[i].row_len == 0 && segs[i].numel)
+      return fail(COADAPT_E_VALIDATION, "gen segment row_len is 0");
+    coadapt::dev::GenSeg gs{segs[i].local_off, segs[i].numel,
+                            segs[i].global_base, segs[i].row_len,
+                            segs[i].row_stride};
+    CU(coadapt::dev::launch_synth_mean(dst, dtype, gs, seed, sample0, nsamples,
+                                       g0, unit,
+                                       static_cast<cudaStream_t>(stream)));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  return COADAPT_OK;
+}
+
+int coadapt_l2_flush(void* scratch, uint64_t bytes, void* stream) {
+  if (!scratch) return fail(COADAPT_E_VALIDATION, "scratch is NULL");
+  CU(coadapt::dev::launch_l2_flush(scratch, bytes,
+                                   static_cast<cudaStream_t>(stream)));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return COADAPT_OK;
+}
+
+int coadapt_read_probe(const void* buf, uint64_t bytes, double* sink,
+                       void* stream) {
+  if (!buf || !sink) return fail(COADAPT_E_VALIDATION, "NULL argument");
+  if (reinterpret_cast<uintptr_t>(buf) & 15)
+    return fail(COADAPT_E_VALIDATION, "probe buffer must be 16B aligned");
+  CU(coadapt::dev::launch_read_probe(buf, bytes, sink,
+                                     static_cast<cudaStream_t>(stream)));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return COADAPT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// internal.h — shared between the kernels (kernels.cu) and the C-ABI layer
+// (cabi.cu).  Not installed; the public boundary is include/coadapt_cuda.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace coadapt {
+namespace dev {
+
+// One maximal run of same-weight, non-zero-weight bucket elements.
+// cum_begin is its first index in the "active" (compacted) element space.
+struct Range {
+  uint64_t abs_begin;
+  uint64_t cum_begin;
+  uint64_t len;
+  double weight;
+};
+
+constexpr int kMaxBatch = 64;  // buckets per batched launch
+constexpr int kMaxFusedM = 16; // micro-buckets per fused launch
+
+struct BatchArgs {
+  const void* ptr[kMaxBatch];
+  int32_t slot[kMaxBatch];
+  int32_t count;
+};
+
+struct FusedArgs {
+  const void* ptr[kMaxFusedM];
+  int32_t slot0;     // slot of s_{dp, 0}
+  int32_t gslot;     // slot of gbar^2
+  double gscale;     // 1 / M^2
+};
+
+// Where a reduction writes: per-CTA partials, the ticket of the last-block
+// combine, and the accumulator slots it adds into.
+struct Sink {
+  double* partials;
+  unsigned int* ticket;
+  double* slots;
+};
+
+// Compacted-space window [e_begin, e_end) that one launch covers, and the
+// pointer offset that maps abs element index -> address (base - w0*es).
+struct Window {
+  uint64_t e_begin;
+  uint64_t e_end;
+};
+
+// Kernel launchers.  Return cudaSuccess or the launch error.  `grid` is
+// computed by the caller from grid_for().
+cudaError_t launch_sqnorm_batched(int dtype, const Range* ranges, int nranges,
+                                  Window w, const BatchArgs& jobs, Sink sink,
+                                  int grid, cudaStream_t s);
+cudaError_t launch_fused(int dtype, int M, const Range* ranges, int nranges,
+                         Window w, const FusedArgs& args, Sink sink, int grid,
+                         cudaStream_t s);
+// max resident CTAs per SM for the kernel that launch_* would pick
+int occupancy_sqnorm(int dtype);
+int occupancy_fused(int dtype, int M);
+int threads_sqnorm();
+int threads_fused(int M);
+
+struct FinalizeArgs {
+  const double* slots;
+  int32_t n;               // N; slots[N] = gbar^2
+  int64_t global_batch;
+  int64_t tokens;
+  void* state;             // coadapt_gns_state*
+  void* result;            // coadapt_gns_result*
+};
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t s);
+
+struct GenSeg {
+  uint64_t local_off, numel, global_base, row_len, row_stride;
+};
+cudaError_t launch_synth(void* dst, int dtype, GenSeg seg, uint64_t seed,
+                         uint64_t sample, float g0, float unit,
+                         cudaStream_t s);
+cudaError_t launch_synth_mean(void* dst, int dtype, GenSeg seg, uint64_t seed,
+                              uint64_t sample0, int64_t nsamples, float g0,
+                              float unit, cudaStream_t s);
+cudaError_t launch_l2_flush(void* buf, uint64_t bytes, cudaStream_t s);
+cudaError_t launch_read_probe(const void* buf, uint64_t bytes, double* sink,
+                              cudaStream_t s);
+
+}  // namespace dev
+}  // namespace coadapt

@@ -1,0 +1,791 @@
+// kernels.cu — sm_100a kernels of the GNS hot path.
+//
+//   K1  sqnorm_kernel  : s += sum_ranges w * ||bucket[range]||^2 for a batch
+//                        of buckets sharing one layout, and
+//                        the d > 1 mean-gradient read.
+//   K1f fused_kernel   : d = 1: all M micro-buckets of a rank in one pass,
+//                        every s_m plus ||sum_m g_m||^2 (no second read).
+//   K3  finalize_kernel: finalize_step + update_ema + gns (gns.hpp:42-73).
+//   K0  synth kernels  : integer-exact synthetic gradients (test/bench data).
+//
+// Bandwidth design (B200, HBM3e): the reductions are pure streams.  Each CTA
+// owns one contiguous, equal share of the bucket's active elements (perfect
+// byte balance, DRAM-page friendly), walks it with 128-bit
+// ld.global.nc.L1::no_allocate loads, U independent loads in flight per
+// thread, and several CTAs per SM, so that ~100+ KB per SM is in flight
+// (Little's law at ~7 TB/s x ~1 us needs ~45 KB/SM).  Weight-0 ranges (TP
+// duplicates) are never loaded.  Squares of bf16/fp16 are exact in fp32;
+// each 16-byte vector's 8 squares are summed in fp32 and promoted once to
+// the thread's fp64 accumulator; fp32/fp64 inputs square in fp64.  CTA
+// partials are combined by the last CTA in a fixed order, so results are
+// bit-reproducible run to run.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/coadapt_cuda.h"
+#include "internal.h"
+
+namespace coadapt {
+namespace dev {
+namespace {
+
+template <int DT>
+struct Elem;
+template <>
+struct Elem<COADAPT_BF16> {
+  static constexpr int kSize = 2, kPerVec = 8;
+};
+template <>
+struct Elem<COADAPT_FP16> {
+  static constexpr int kSize = 2, kPerVec = 8;
+};
+template <>
+struct Elem<COADAPT_FP32> {
+  static constexpr int kSize = 4, kPerVec = 4;
+};
+template <>
+struct Elem<COADAPT_FP64> {
+  static constexpr int kSize = 8, kPerVec = 2;
+};
+
+// Streaming 128-bit load: read-only path, no L1 allocation, 256B L2 prefetch.
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) {
+  return __uint_as_float(w << 16);
+}
+__device__ __forceinline__ float bf16_hi(uint32_t w) {
+  return __uint_as_float(w & 0xffff0000u);
+}
+
+// The 8/4/2 element values of one 16-byte vector as fp32 (not for fp64).
+template <int DT>
+__device__ __forceinline__ void unpack(const uint4& v, float* f);
+template <>
+__device__ __forceinline__ void unpack<COADAPT_BF16>(const uint4& v,
+                                                     float* f) {
+  f[0] = bf16_lo(v.x); f[1] = bf16_hi(v.x);
+  f[2] = bf16_lo(v.y); f[3] = bf16_hi(v.y);
+  f[4] = bf16_lo(v.z); f[5] = bf16_hi(v.z);
+  f[6] = bf16_lo(v.w); f[7] = bf16_hi(v.w);
+}
+template <>
+__device__ __forceinline__ void unpack<COADAPT_FP16>(const uint4& v,
+                                                     float* f) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+    float2 t = __half22float2(h);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+template <>
+__device__ __forceinline__ void unpack<COADAPT_FP32>(const uint4& v,
+                                                     float* f) {
+  f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+  f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+}
+
+// acc += sum of squares of one vector.
+template <int DT>
+__device__ __forceinline__ void vacc(const uint4& v, double& acc) {
+  if constexpr (DT == COADAPT_BF16 || DT == COADAPT_FP16) {
+    float f[8];
+    unpack<DT>(v, f);
+    // each square is exact in fp32 (<= 22 significant bits); two chains
+    float s0 = f[0] * f[0], s1 = f[1] * f[1];
+    s0 = fmaf(f[2], f[2], s0); s1 = fmaf(f[3], f[3], s1);
+    s0 = fmaf(f[4], f[4], s0); s1 = fmaf(f[5], f[5], s1);
+    s0 = fmaf(f[6], f[6], s0); s1 = fmaf(f[7], f[7], s1);
+    const float p = s0 + s1;
+    // fp32 is safe when the partial is finite and >= 2^-100 (subnormal
+    // squares then perturb it by < 2^-47 relative).  Otherwise (|x| near
+    // the fp32-square overflow/underflow limits, Inf/NaN) redo the vector
+    // in fp64; exact zero vectors skip both.
+    if (p >= 0x1p-100f && p <= 3.402823466e38f) {
+      acc += (double)p;
+    } else if (((v.x | v.y | v.z | v.w) & 0x7fff7fffu) != 0u) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double d = f[i];
+        acc = fma(d, d, acc);
+      }
+    }
+  } else if constexpr (DT == COADAPT_FP32) {
+    float f[4];
+    unpack<DT>(v, f);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double d = f[i];
+      acc = fma(d, d, acc);
+    }
+  } else {
+    const double a = __hiloint2double(v.y, v.x);
+    const double b = __hiloint2double(v.w, v.z);
+    acc = fma(a, a, acc);
+    acc = fma(b, b, acc);
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ double elem_f64(uintptr_t addr) {
+  if constexpr (DT == COADAPT_BF16) {
+    const uint16_t h = *reinterpret_cast<const uint16_t*>(addr);
+    return (double)__uint_as_float((uint32_t)h << 16);
+  } else if constexpr (DT == COADAPT_FP16) {
+    return (double)__half2float(*reinterpret_cast<const __half*>(addr));
+  } else if constexpr (DT == COADAPT_FP32) {
+    return (double)*reinterpret_cast<const float*>(addr);
+  } else {
+    return *reinterpret_cast<const double*>(addr);
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ float elem_f32(uintptr_t addr) {
+  if constexpr (DT == COADAPT_BF16) {
+    const uint16_t h = *reinterpret_cast<const uint16_t*>(addr);
+    return __uint_as_float((uint32_t)h << 16);
+  } else if constexpr (DT == COADAPT_FP16) {
+    return __half2float(*reinterpret_cast<const __half*>(addr));
+  } else {
+    return *reinterpret_cast<const float*>(addr);
+  }
+}
+
+// ---------------------------------------------------------------- reductions
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();  // red may still be read by a previous call
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  v = 0.0;
+  if (warp == 0) {
+    v = lane < NT / 32 ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  }
+  return v;  // valid in thread 0
+}
+
+// Last-CTA combine: every CTA has stored its per-output partial at
+// partials[o * G + cta]; the CTA that takes the last ticket sums each
+// output's G partials in a fixed order and adds scale*sum into slots[slot].
+template <int NT>
+__device__ __forceinline__ void last_cta_combine(const Sink& sink, int nout,
+                                                 const int32_t* out_slot,
+                                                 const double* out_scale,
+                                                 double* red) {
+  __shared__ unsigned int is_last;
+  const int G = gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int t = atomicAdd(sink.ticket, 1u);
+    is_last = (t == (unsigned)G - 1u);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int o = 0; o < nout; ++o) {
+    double v = 0.0;
+    for (int c = threadIdx.x; c < G; c += NT)
+      v += __ldcg(sink.partials + (size_t)o * G + c);
+    v = block_sum<NT>(v, red);
+    if (threadIdx.x == 0) {
+      const double sc = out_scale ? out_scale[o] : 1.0;
+      double* dst = sink.slots + out_slot[o];
+      *dst = *dst + (sc == 1.0 ? v : v * sc);
+    }
+  }
+  if (threadIdx.x == 0) *sink.ticket = 0u;  // ready for the next launch
+}
+
+// This CTA's equal share of the window [e_begin, e_end) of active elements,
+// rounded to 64-element multiples so bodies stay 16B-aligned.
+__device__ __forceinline__ void cta_share(const Window& w, uint64_t& e0,
+                                          uint64_t& e1) {
+  const uint64_t n = w.e_end - w.e_begin;
+  uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+  per = (per + 63) & ~uint64_t(63);
+  e0 = w.e_begin + min(n, per * blockIdx.x);
+  e1 = w.e_begin + min(n, per * (blockIdx.x + 1));
+}
+
+__device__ __forceinline__ int find_range(const Range* __restrict__ R, int nr,
+                                          uint64_t e) {
+  int lo = 0, hi = nr - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (R[mid].cum_begin <= e) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// acc += ||x[a, a+n)||^2 of one stream.
+template <int DT, int NT, int U>
+__device__ __forceinline__ void piece_sumsq(uintptr_t base, uint64_t a,
+                                            uint64_t n, double& acc) {
+  constexpr int ES = Elem<DT>::kSize;
+  const uintptr_t u0 = base + a * ES, u1 = u0 + n * ES;
+  const uintptr_t v0 = (u0 + 15) & ~uintptr_t(15), v1 = u1 & ~uintptr_t(15);
+  const unsigned tid = threadIdx.x;
+  if (v0 >= v1) {
+    for (uint64_t i = tid; i < n; i += NT) {
+      const double x = elem_f64<DT>(u0 + i * ES);
+      acc = fma(x, x, acc);
+    }
+    return;
+  }
+  const unsigned nhead = (unsigned)((v0 - u0) / ES);
+  const unsigned ntail = (unsigned)((u1 - v1) / ES);
+  if (tid < nhead) {
+    const double x = elem_f64<DT>(u0 + tid * ES);
+    acc = fma(x, x, acc);
+  }
+  if (tid < ntail) {
+    const double x = elem_f64<DT>(v1 + tid * ES);
+    acc = fma(x, x, acc);
+  }
+  const uint4* __restrict__ vp = reinterpret_cast<const uint4*>(v0);
+  const uint64_t nv = (v1 - v0) >> 4;
+  uint64_t i = tid;
+  for (; i + (uint64_t)(U - 1) * NT < nv; i += (uint64_t)U * NT) {
+    uint4 r[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) r[j] = ld_stream(vp + i + (uint64_t)j * NT);
+#pragma unroll
+    for (int j = 0; j < U; ++j) vacc<DT>(r[j], acc);
+  }
+  for (; i < nv; i += NT) vacc<DT>(ld_stream(vp + i), acc);
+}
+
+// ---------------------------------------------------------------- K1
+
+template <int DT, int NT, int U>
+__global__ void __launch_bounds__(NT, 4)
+    sqnorm_kernel(const Range* __restrict__ R, int nr, Window w,
+                  const BatchArgs jobs, Sink sink) {
+  __shared__ double red[32];
+  uint64_t e0, e1;
+  cta_share(w, e0, e1);
+  const int k0 = (e0 < e1) ? find_range(R, nr, e0) : nr;
+  for (int b = 0; b < jobs.count; ++b) {
+    const uintptr_t base = reinterpret_cast<uintptr_t>(jobs.ptr[b]);
+    double total = 0.0;
+    for (int k = k0; k < nr && R[k].cum_begin < e1; ++k) {
+      const uint64_t cb = R[k].cum_begin, ce = cb + R[k].len;
+      const uint64_t s = cb > e0 ? cb : e0, e = ce < e1 ? ce : e1;
+      if (s >= e) continue;
+      double acc = 0.0;
+      piece_sumsq<DT, NT, U>(base, R[k].abs_begin + (s - cb), e - s, acc);
+      total += R[k].weight == 1.0 ? acc : R[k].weight * acc;
+    }
+    total = block_sum<NT>(total, red);
+    if (threadIdx.x == 0)
+      sink.partials[(size_t)b * gridDim.x + blockIdx.x] = total;
+  }
+  last_cta_combine<NT>(sink, jobs.count, jobs.slot, nullptr, red);
+}
+
+// ---------------------------------------------------------------- K1f
+
+// M streams at the same element positions (all M pointers are congruent
+// mod 16, checked by the host).  acc[m] += x_m^2; gacc += (sum_m x_m)^2
+// with the sum in fp32, micro-batches in order (Megatron main_grad).
+template <int DT, int M, int NT, int UP>
+__device__ __forceinline__ void fused_piece(const FusedArgs& args, uint64_t a,
+                                            uint64_t n, double* acc,
+                                            double& gacc) {
+  constexpr int ES = Elem<DT>::kSize;
+  constexpr int PV = Elem<DT>::kPerVec;
+  const uintptr_t b0 = reinterpret_cast<uintptr_t>(args.ptr[0]);
+  const uintptr_t u0 = b0 + a * ES, u1 = u0 + n * ES;
+  uintptr_t v0 = (u0 + 15) & ~uintptr_t(15);
+  uintptr_t v1 = u1 & ~uintptr_t(15);
+  const unsigned tid = threadIdx.x;
+  auto scalar = [&](uint64_t i) {  // element at u0-relative byte offset i
+    float sum = 0.0f;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uintptr_t p =
+          reinterpret_cast<uintptr_t>(args.ptr[m]) + (u0 - b0) + i;
+      const float x = elem_f32<DT>(p);
+      const double xd = x;
+      acc[m] = fma(xd, xd, acc[m]);
+      sum = __fadd_rn(sum, x);
+    }
+    const double sd = sum;
+    gacc = fma(sd, sd, gacc);
+  };
+  if (v0 >= v1) {
+    for (uint64_t i = tid; i < n; i += NT) scalar(i * ES);
+    return;
+  }
+  const unsigned nhead = (unsigned)((v0 - u0) / ES);
+  const unsigned ntail = (unsigned)((u1 - v1) / ES);
+  if (tid < nhead) scalar((uint64_t)tid * ES);
+  if (tid < ntail) scalar((v1 - u0) + (uint64_t)tid * ES);
+  const uint64_t nv = (v1 - v0) >> 4;
+  const uint64_t voff = v0 - b0;  // byte offset of the first vector
+  uint64_t i = tid;
+  for (; i + (uint64_t)(UP - 1) * NT < nv; i += (uint64_t)UP * NT) {
+    uint4 r[UP][M];
+#pragma unroll
+    for (int p = 0; p < UP; ++p)
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+        r[p][m] = ld_stream(reinterpret_cast<const uint4*>(
+            reinterpret_cast<uintptr_t>(args.ptr[m]) + voff +
+            (i + (uint64_t)p * NT) * 16));
+#pragma unroll
+    for (int p = 0; p < UP; ++p) {
+      float sum[PV];
+#pragma unroll
+      for (int e = 0; e < PV; ++e) sum[e] = 0.0f;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        float f[PV];
+        unpack<DT>(r[p][m], f);
+        vacc<DT>(r[p][m], acc[m]);
+#pragma unroll
+        for (int e = 0; e < PV; ++e) sum[e] = __fadd_rn(sum[e], f[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < PV; ++e) {
+        const double sd = sum[e];
+        gacc = fma(sd, sd, gacc);
+      }
+    }
+  }
+  for (; i < nv; i += NT) {
+    float sum[PV];
+#pragma unroll
+    for (int e = 0; e < PV; ++e) sum[e] = 0.0f;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uint4 v = ld_stream(reinterpret_cast<const uint4*>(
+          reinterpret_cast<uintptr_t>(args.ptr[m]) + voff + i * 16));
+      float f[PV];
+      unpack<DT>(v, f);
+      vacc<DT>(v, acc[m]);
+#pragma unroll
+      for (int e = 0; e < PV; ++e) sum[e] = __fadd_rn(sum[e], f[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < PV; ++e) {
+      const double sd = sum[e];
+      gacc = fma(sd, sd, gacc);
+    }
+  }
+}
+
+template <int DT, int M, int NT, int UP>
+__global__ void __launch_bounds__(NT)
+    fused_kernel(const Range* __restrict__ R, int nr, Window w,
+                 const FusedArgs args, Sink sink) {
+  __shared__ double red[32];
+  __shared__ int32_t out_slot[M + 1];
+  __shared__ double out_scale[M + 1];
+  uint64_t e0, e1;
+  cta_share(w, e0, e1);
+  double total[M], gtotal = 0.0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) total[m] = 0.0;
+  if (e0 < e1) {
+    for (int k = find_range(R, nr, e0); k < nr && R[k].cum_begin < e1; ++k) {
+      const uint64_t cb = R[k].cum_begin, ce = cb + R[k].len;
+      const uint64_t s = cb > e0 ? cb : e0, e = ce < e1 ? ce : e1;
+      if (s >= e) continue;
+      double acc[M], gacc = 0.0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) acc[m] = 0.0;
+      fused_piece<DT, M, NT, UP>(args, R[k].abs_begin + (s - cb), e - s, acc,
+                                 gacc);
+      const double wt = R[k].weight;
+#pragma unroll
+      for (int m = 0; m < M; ++m) total[m] += wt == 1.0 ? acc[m] : wt * acc[m];
+      gtotal += wt == 1.0 ? gacc : wt * gacc;
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const double v = block_sum<NT>(total[m], red);
+    if (threadIdx.x == 0)
+      sink.partials[(size_t)m * gridDim.x + blockIdx.x] = v;
+  }
+  {
+    const double v = block_sum<NT>(gtotal, red);
+    if (threadIdx.x == 0)
+      sink.partials[(size_t)M * gridDim.x + blockIdx.x] = v;
+  }
+  if (threadIdx.x <= M) {
+    out_slot[threadIdx.x] =
+        threadIdx.x < M ? args.slot0 + (int)threadIdx.x : args.gslot;
+    out_scale[threadIdx.x] = threadIdx.x < M ? 1.0 : args.gscale;
+  }
+  last_cta_combine<NT>(sink, M + 1, out_slot, out_scale, red);
+}
+
+// ---------------------------------------------------------------- K3
+
+struct DevState {  // == coadapt_gns_state
+  double ema_signal, ema_noise, alpha_early, alpha_late;
+  int64_t phase_boundary_tokens, tokens_seen;
+  double calibration;
+  int32_t initialized, reserved_;
+};
+struct DevResult {  // == coadapt_gns_result
+  double signal, noise, noise_raw, mean_grad_sq;
+  DevState state;
+  double phi, b_simple;
+  int64_t sample_count;
+  int32_t phi_available, status;
+};
+static_assert(sizeof(DevState) == sizeof(coadapt_gns_state), "layout");
+static_assert(sizeof(DevResult) == sizeof(coadapt_gns_result), "layout");
+
+// Single thread, explicit round-to-nearest intrinsics: no FMA contraction,
+// so every value is bit-identical to the host C++ formulas
+// (gns.hpp:42-44, 64-66, 70-72).
+__global__ void finalize_kernel(FinalizeArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  DevState* st = static_cast<DevState*>(a.state);
+  DevResult* res = static_cast<DevResult*>(a.result);
+  const int n = a.n;
+  double sum = 0.0;
+  bool ok = n >= 2;
+  for (int i = 0; i < n; ++i) {
+    const double s = a.slots[i];
+    ok = ok && (s >= 0.0) && isfinite(s);  // gns.hpp:19: negative rejected
+    sum = __dadd_rn(sum, s);
+  }
+  const double g2 = a.slots[n];
+  ok = ok && (g2 >= 0.0) && isfinite(g2);
+  res->sample_count = n;
+  if (!ok) {
+    res->status = COADAPT_E_VALIDATION;
+    res->state = *st;
+    res->phi_available = 0;
+    res->phi = __longlong_as_double(0x7ff8000000000000ll);
+    res->signal = res->noise = res->noise_raw = 0.0;
+    res->mean_grad_sq = g2;
+    res->b_simple = res->phi;
+    return;
+  }
+  const double N = (double)n;
+  const double nm1 = __dsub_rn(N, 1.0);
+  const double sbar = __ddiv_rn(sum, N);
+  const double signal = __ddiv_rn(__dsub_rn(__dmul_rn(N, g2), sbar), nm1);
+  const double noise_raw = __ddiv_rn(
+      __dmul_rn(__dsub_rn(sbar, g2), (double)a.global_batch), nm1);
+  const double noise = noise_raw > 0.0 ? noise_raw : 0.0;
+  // update_ema: alpha from tokens_seen before the increment
+  DevState s = *st;
+  const double alpha =
+      s.tokens_seen < s.phase_boundary_tokens ? s.alpha_early : s.alpha_late;
+  if (!s.initialized) {
+    s.ema_signal = signal;
+    s.ema_noise = noise;
+    s.initialized = 1;
+  } else {
+    const double beta = __dsub_rn(1.0, alpha);
+    s.ema_signal =
+        __dadd_rn(__dmul_rn(alpha, s.ema_signal), __dmul_rn(beta, signal));
+    s.ema_noise =
+        __dadd_rn(__dmul_rn(alpha, s.ema_noise), __dmul_rn(beta, noise));
+  }
+  if (s.ema_noise < 0.0) s.ema_noise = 0.0;
+  s.tokens_seen += a.tokens;
+  *st = s;
+  res->signal = signal;
+  res->noise = noise;
+  res->noise_raw = noise_raw;
+  res->mean_grad_sq = g2;
+  res->state = s;
+  res->status = COADAPT_OK;
+  res->b_simple = __ddiv_rn(noise, signal);
+  if (s.ema_signal > 0.0) {
+    res->phi = __ddiv_rn(__dmul_rn(s.calibration, s.ema_noise), s.ema_signal);
+    res->phi_available = 1;
+  } else {
+    res->phi = __longlong_as_double(0x7ff8000000000000ll);
+    res->phi_available = 0;
+  }
+}
+
+// ---------------------------------------------------------------- K0
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__host__ __device__ inline uint64_t mix64_h(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+inline uint64_t sample_key(uint64_t seed, uint64_t sample) {
+  return mix64_h(seed ^ mix64_h(sample + 0x632BE59BD9B4E019ull));
+}
+inline uint64_t sign_key(uint64_t seed) {
+  return mix64_h(seed ^ 0xA0761D6478BD642Full);
+}
+
+__device__ __forceinline__ float synth_value(uint64_t skey, uint64_t gkey,
+                                             uint64_t gidx, float g0,
+                                             float unit) {
+  const uint64_t h = mix64(skey ^ gidx);
+  const int32_t ih = (int32_t)((h & 0xffff) + ((h >> 16) & 0xffff) +
+                               ((h >> 32) & 0xffff) + (h >> 48)) -
+                     131070;
+  const float zeta = __fmul_rn((float)ih, unit);
+  const float g = (mix64(gkey ^ gidx) >> 63) ? -g0 : g0;
+  return __fadd_rn(g, zeta);
+}
+
+__device__ __forceinline__ void store_elem(void* dst, int dtype, uint64_t i,
+                                           float v) {
+  if (dtype == COADAPT_BF16)
+    reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(v);
+  else if (dtype == COADAPT_FP16)
+    reinterpret_cast<__half*>(dst)[i] = __float2half_rn(v);
+  else if (dtype == COADAPT_FP32)
+    reinterpret_cast<float*>(dst)[i] = v;
+  else
+    reinterpret_cast<double*>(dst)[i] = (double)v;
+}
+
+__device__ __forceinline__ float round_trip(int dtype, float v) {
+  if (dtype == COADAPT_BF16) return __bfloat162float(__float2bfloat16_rn(v));
+  if (dtype == COADAPT_FP16) return __half2float(__float2half_rn(v));
+  return v;
+}
+
+__global__ void synth_kernel(void* dst, int dtype, GenSeg seg, uint64_t skey,
+                             uint64_t gkey, float g0, float unit) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+       j < seg.numel; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t gidx = seg.global_base + (j / seg.row_len) * seg.row_stride +
+                          (j % seg.row_len);
+    store_elem(dst, dtype, seg.local_off + j,
+               synth_value(skey, gkey, gidx, g0, unit));
+  }
+}
+
+__global__ void synth_mean_kernel(void* dst, int dtype, GenSeg seg,
+                                  uint64_t seed, uint64_t sample0,
+                                  int64_t nsamples, uint64_t gkey, float g0,
+                                  float unit, float inv_n) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+       j < seg.numel; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t gidx = seg.global_base + (j / seg.row_len) * seg.row_stride +
+                          (j % seg.row_len);
+    float acc = 0.0f;
+    for (int64_t n = 0; n < nsamples; ++n) {
+      const uint64_t skey =
+          mix64(seed ^ mix64(sample0 + (uint64_t)n + 0x632BE59BD9B4E019ull));
+      acc = __fadd_rn(acc,
+                      round_trip(dtype, synth_value(skey, gkey, gidx, g0, unit)));
+    }
+    store_elem(dst, dtype, seg.local_off + j, __fmul_rn(acc, inv_n));
+  }
+}
+
+__global__ void l2_flush_kernel(uint4* buf, uint64_t nvec, uint32_t salt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    buf[i] = make_uint4(salt, (uint32_t)i, salt, (uint32_t)(i >> 32));
+}
+
+// read-only streaming probe: the same load pattern as K1 without the math
+template <int NT, int U>
+__global__ void __launch_bounds__(NT)
+    read_probe_kernel(const uint4* __restrict__ p, uint64_t nvec,
+                      double* sink) {
+  uint32_t x = 0;
+  const uint64_t per = (nvec + gridDim.x - 1) / gridDim.x;
+  const uint64_t b = per * blockIdx.x, e = min(nvec, b + per);
+  uint64_t i = b + threadIdx.x;
+  for (; i + (uint64_t)(U - 1) * NT < e; i += (uint64_t)U * NT) {
+    uint4 r[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) r[j] = ld_stream(p + i + (uint64_t)j * NT);
+#pragma unroll
+    for (int j = 0; j < U; ++j) x ^= r[j].x ^ r[j].y ^ r[j].z ^ r[j].w;
+  }
+  for (; i < e; i += NT) {
+    const uint4 r = ld_stream(p + i);
+    x ^= r.x ^ r.y ^ r.z ^ r.w;
+  }
+  if (x == 0x9e3779b9u) *sink = (double)x;  // keeps the loads alive
+}
+
+// ---------------------------------------------------------------- configs
+
+constexpr int kNT = 256;   // threads per CTA, K1
+constexpr int kU = 8;      // 16-byte loads in flight per thread, K1
+constexpr int kNTF = 256;  // threads per CTA, K1f
+
+template <int M>
+struct FusedCfg {
+  // keep ~8-16 loads of 16 B in flight per thread
+  static constexpr int UP = M >= 8 ? 1 : (M >= 4 ? 2 : (M >= 2 ? 4 : 8));
+};
+
+template <int DT>
+void* sqnorm_fn() {
+  return reinterpret_cast<void*>(&sqnorm_kernel<DT, kNT, kU>);
+}
+
+template <int DT, int M>
+void* fused_fn() {
+  return reinterpret_cast<void*>(&fused_kernel<DT, M, kNTF, FusedCfg<M>::UP>);
+}
+
+template <int DT>
+void* fused_fn_rt(int M) {
+  switch (M) {
+#define F(m) \
+  case m:    \
+    return fused_fn<DT, m>();
+    F(1) F(2) F(3) F(4) F(5) F(6) F(7) F(8) F(9) F(10) F(11) F(12) F(13) F(14)
+        F(15) F(16)
+#undef F
+  }
+  return nullptr;
+}
+
+void* fused_kernel_ptr(int dtype, int M) {
+  switch (dtype) {
+    case COADAPT_BF16: return fused_fn_rt<COADAPT_BF16>(M);
+    case COADAPT_FP16: return fused_fn_rt<COADAPT_FP16>(M);
+    case COADAPT_FP32: return fused_fn_rt<COADAPT_FP32>(M);
+  }
+  return nullptr;
+}
+
+void* sqnorm_kernel_ptr(int dtype) {
+  switch (dtype) {
+    case COADAPT_BF16: return sqnorm_fn<COADAPT_BF16>();
+    case COADAPT_FP16: return sqnorm_fn<COADAPT_FP16>();
+    case COADAPT_FP32: return sqnorm_fn<COADAPT_FP32>();
+    case COADAPT_FP64: return sqnorm_fn<COADAPT_FP64>();
+  }
+  return nullptr;
+}
+
+int occupancy_of(void* fn, int nt) {
+  int occ = 0;
+  if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, 0) !=
+                 cudaSuccess)
+    return 0;
+  return occ;
+}
+
+}  // namespace
+
+int threads_sqnorm() { return kNT; }
+int threads_fused(int) { return kNTF; }
+int occupancy_sqnorm(int dtype) {
+  return occupancy_of(sqnorm_kernel_ptr(dtype), kNT);
+}
+int occupancy_fused(int dtype, int M) {
+  return occupancy_of(fused_kernel_ptr(dtype, M), kNTF);
+}
+
+cudaError_t launch_sqnorm_batched(int dtype, const Range* ranges, int nranges,
+                                  Window w, const BatchArgs& jobs, Sink sink,
+                                  int grid, cudaStream_t s) {
+  void* fn = sqnorm_kernel_ptr(dtype);
+  if (!fn) return cudaErrorInvalidValue;
+  void* args[] = {(void*)&ranges, (void*)&nranges, (void*)&w, (void*)&jobs,
+                  (void*)&sink};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(kNT), args, 0, s);
+}
+
+cudaError_t launch_fused(int dtype, int M, const Range* ranges, int nranges,
+                         Window w, const FusedArgs& fa, Sink sink, int grid,
+                         cudaStream_t s) {
+  void* fn = fused_kernel_ptr(dtype, M);
+  if (!fn) return cudaErrorInvalidValue;
+  void* args[] = {(void*)&ranges, (void*)&nranges, (void*)&w, (void*)&fa,
+                  (void*)&sink};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(kNTF), args, 0, s);
+}
+
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
+  finalize_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+static int grid_for_elems(uint64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t want = (n + 255) / 256;
+  const uint64_t cap = (uint64_t)sms * 16;
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+cudaError_t launch_synth(void* dst, int dtype, GenSeg seg, uint64_t seed,
+                         uint64_t sample, float g0, float unit,
+                         cudaStream_t s) {
+  if (seg.numel == 0) return cudaSuccess;
+  synth_kernel<<<grid_for_elems(seg.numel), 256, 0, s>>>(
+      dst, dtype, seg, sample_key(seed, sample), sign_key(seed), g0, unit);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_mean(void* dst, int dtype, GenSeg seg, uint64_t seed,
+                              uint64_t sample0, int64_t nsamples, float g0,
+                              float unit, cudaStream_t s) {
+  if (seg.numel == 0) return cudaSuccess;
+  const float inv_n = (float)(1.0 / (double)nsamples);
+  synth_mean_kernel<<<grid_for_elems(seg.numel), 256, 0, s>>>(
+      dst, dtype, seg, seed, sample0, nsamples, sign_key(seed), g0, unit,
+      inv_n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l2_flush(void* buf, uint64_t bytes, cudaStream_t s) {
+  static uint32_t salt = 1;
+  const uint64_t nvec = bytes / 16;
+  if (!nvec) return cudaSuccess;
+  l2_flush_kernel<<<grid_for_elems(nvec), 256, 0, s>>>(
+      static_cast<uint4*>(buf), nvec, salt++);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_read_probe(const void* buf, uint64_t bytes, double* sink,
+                              cudaStream_t s) {
+  int dev = 0, sms = 148, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ, read_probe_kernel<kNT, kU>, kNT, 0);
+  if (occ < 1) occ = 1;
+  read_probe_kernel<kNT, kU><<<sms * occ, kNT, 0, s>>>(
+      static_cast<const uint4*>(buf), bytes / 16, sink);
+  return cudaGetLastError();
+}
+
+}  // namespace dev
+}  // namespace coadapt

@@ -1,0 +1,227 @@
+"""Device (B200) GNS path: Python handles over the C-ABI of include/coadapt_cuda.h.
+
+``BucketPlan`` compiles a rank's gradient-bucket layout (segments with dedup
+weights); ``GnsDevice`` is the device-resident StepAccumulator + GnsState of
+one optimizer step (gns.hpp:15-73): squared-norm reductions accumulate into
+its N+1 fp64 slots, ``allreduce`` sums the slots over ranks with NCCL, and
+``finalize`` runs finalize_step + update_ema + gns in a device kernel.
+Tensors are passed by pointer; PyTorch is used only for memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import GnsResult, GnsState, check, lib
+
+TORCH_TO_DTYPE = {torch.bfloat16: L.BF16, torch.float16: L.FP16, torch.float32: L.FP32,
+                  torch.float64: L.FP64}
+DTYPE_TO_TORCH = {v: k for k, v in TORCH_TO_DTYPE.items()}
+ESIZE = {L.BF16: 2, L.FP16: 2, L.FP32: 4, L.FP64: 8}
+
+
+def _ptr(x) -> int:
+    if isinstance(x, torch.Tensor):
+        return x.data_ptr()
+    return int(x)
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _seg_array(segments) -> tuple:
+    segs = list(segments)
+    arr = (L.Segment * max(1, len(segs)))(*[L.Segment(int(o), int(n), float(w)) for o, n, w in segs])
+    return arr, len(segs)
+
+
+def _gen_array(gsegs) -> tuple:
+    gs = list(gsegs)
+    arr = (L.GenSegment * max(1, len(gs)))(*[L.GenSegment(*map(int, g)) for g in gs])
+    return arr, len(gs)
+
+
+class BucketPlan:
+    """A rank's flattened bucket layout: [(offset, numel, weight)] in elements."""
+
+    def __init__(self, segments, bucket_numel: int, dtype: int, device: int = 0,
+                 slice_index: Optional[int] = None, slice_count: Optional[int] = None):
+        arr, n = _seg_array(segments)
+        h = C.c_void_p()
+        if slice_count is None:
+            check(lib().coadapt_plan_create(arr, n, int(bucket_numel), int(dtype), int(device), C.byref(h)))
+        else:
+            check(lib().coadapt_plan_create_slice(arr, n, int(bucket_numel), int(dtype), int(device),
+                                                  int(slice_index), int(slice_count), C.byref(h)))
+        self.handle = h
+        self.dtype = int(dtype)
+        self.bucket_numel = int(bucket_numel)
+        self.device = int(device)
+
+    @property
+    def active_elements(self) -> int:
+        a, r = C.c_uint64(), C.c_uint64()
+        check(lib().coadapt_plan_info(self.handle, C.byref(a), C.byref(r)))
+        return a.value
+
+    @property
+    def num_ranges(self) -> int:
+        a, r = C.c_uint64(), C.c_uint64()
+        check(lib().coadapt_plan_info(self.handle, C.byref(a), C.byref(r)))
+        return r.value
+
+    @property
+    def active_bytes(self) -> int:
+        return self.active_elements * ESIZE[self.dtype]
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().coadapt_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GnsDevice:
+    """Device StepAccumulator (gns.hpp:15-32) + GnsState (gns.hpp:53-62)."""
+
+    def __init__(self, dp_size: int, micro_count: int, global_batch: int, device: int = 0):
+        h = C.c_void_p()
+        check(lib().coadapt_gns_create(int(dp_size), int(micro_count), int(global_batch), int(device),
+                                       C.byref(h)))
+        self.handle = h
+        self.dp_size, self.micro_count, self.global_batch = int(dp_size), int(micro_count), int(global_batch)
+        self.device = int(device)
+
+    @property
+    def n(self) -> int:
+        return self.dp_size * self.micro_count
+
+    def reshape(self, dp_size: int, micro_count: int, global_batch: int) -> None:
+        check(lib().coadapt_gns_reshape(self.handle, int(dp_size), int(micro_count), int(global_batch)))
+        self.dp_size, self.micro_count, self.global_batch = int(dp_size), int(micro_count), int(global_batch)
+
+    def begin_step(self, stream=None) -> None:
+        check(lib().coadapt_gns_begin_step(self.handle, _stream(stream)))
+
+    def micro_sqnorm(self, plan: BucketPlan, bucket, dp_index: int, micro: int, stream=None) -> None:
+        check(lib().coadapt_gns_micro_sqnorm(self.handle, plan.handle, _ptr(bucket), int(dp_index),
+                                             int(micro), _stream(stream)))
+
+    def micro_sqnorm_batched(self, plan: BucketPlan, buckets: Sequence, dp_index: Sequence[int],
+                             micro: Sequence[int], stream=None) -> None:
+        k = len(buckets)
+        ptrs = (C.c_void_p * max(1, k))(*[_ptr(b) for b in buckets])
+        di = (C.c_int32 * max(1, k))(*dp_index)
+        mi = (C.c_int32 * max(1, k))(*micro)
+        check(lib().coadapt_gns_micro_sqnorm_batched(self.handle, plan.handle, ptrs, di, mi, k,
+                                                     _stream(stream)))
+
+    def fused_sqnorm(self, plan: BucketPlan, buckets: Sequence, stream=None) -> None:
+        k = len(buckets)
+        ptrs = (C.c_void_p * max(1, k))(*[_ptr(b) for b in buckets])
+        check(lib().coadapt_gns_fused_sqnorm(self.handle, plan.handle, ptrs, k, _stream(stream)))
+
+    def fused_sqnorm_host(self, plan: BucketPlan, host_buckets: Sequence, stream=None) -> None:
+        k = len(host_buckets)
+        ptrs = (C.c_void_p * max(1, k))(*[_ptr(b) if isinstance(b, torch.Tensor) else b.ctypes.data
+                                          for b in host_buckets])
+        check(lib().coadapt_gns_fused_sqnorm_host(self.handle, plan.handle, ptrs, k, _stream(stream)))
+
+    def mean_sqnorm(self, plan: BucketPlan, mean_grad, stream=None) -> None:
+        check(lib().coadapt_gns_mean_sqnorm(self.handle, plan.handle, _ptr(mean_grad), _stream(stream)))
+
+    def attach_nccl(self, nranks: int, rank: int, unique_id: bytes) -> None:
+        buf = C.create_string_buffer(bytes(unique_id), len(unique_id))
+        check(lib().coadapt_gns_attach_nccl(self.handle, int(nranks), int(rank), buf, len(unique_id)))
+
+    def allreduce(self, stream=None) -> None:
+        check(lib().coadapt_gns_allreduce(self.handle, _stream(stream)))
+
+    def finalize(self, tokens_this_step: int, stream=None) -> None:
+        check(lib().coadapt_gns_finalize(self.handle, int(tokens_this_step), _stream(stream)))
+
+    def result(self) -> GnsResult:
+        r = GnsResult()
+        check(lib().coadapt_gns_read_result(self.handle, C.byref(r)))
+        return r
+
+    def partials(self) -> np.ndarray:
+        out = np.zeros(self.n + 1, np.float64)
+        check(lib().coadapt_gns_read_partials(self.handle, out.ctypes.data, out.size))
+        return out
+
+    def get_state(self) -> GnsState:
+        s = GnsState()
+        check(lib().coadapt_gns_get_state(self.handle, C.byref(s)))
+        return s
+
+    def set_state(self, s: GnsState) -> None:
+        check(lib().coadapt_gns_set_state(self.handle, C.byref(s)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().coadapt_gns_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().coadapt_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+def sqnorm(tensor: torch.Tensor, stream=None) -> float:
+    """||tensor||^2 in fp64 on the device (one-shot K1)."""
+    out = C.c_double()
+    check(lib().coadapt_sqnorm_device(tensor.data_ptr(), tensor.numel(), TORCH_TO_DTYPE[tensor.dtype],
+                                      tensor.device.index or 0, C.byref(out), _stream(stream)))
+    return out.value
+
+
+def synth_fill(out: torch.Tensor, gsegs, seed: int, sample: int, g0: float, noise_unit: float,
+               stream=None) -> None:
+    arr, n = _gen_array(gsegs)
+    check(lib().coadapt_synth_fill(out.data_ptr(), TORCH_TO_DTYPE[out.dtype], arr, n, int(seed),
+                                   int(sample), float(g0), float(noise_unit), _stream(stream)))
+
+
+def synth_mean_fill(out: torch.Tensor, gsegs, seed: int, sample0: int, nsamples: int, g0: float,
+                    noise_unit: float, stream=None) -> None:
+    arr, n = _gen_array(gsegs)
+    check(lib().coadapt_synth_mean_fill(out.data_ptr(), TORCH_TO_DTYPE[out.dtype], arr, n, int(seed),
+                                        int(sample0), int(nsamples), float(g0), float(noise_unit),
+                                        _stream(stream)))
+
+
+def l2_flush(scratch: torch.Tensor, stream=None) -> None:
+    check(lib().coadapt_l2_flush(scratch.data_ptr(), scratch.numel() * scratch.element_size(),
+                                 _stream(stream)))
+
+
+def read_probe(buf: torch.Tensor, sink: torch.Tensor, stream=None) -> None:
+    check(lib().coadapt_read_probe(buf.data_ptr(), buf.numel() * buf.element_size(), sink.data_ptr(),
+                                   _stream(stream)))
+
+
+def kernel_launches() -> int:
+    return int(lib().coadapt_kernel_launches())
