@@ -351,7 +351,7 @@ def run_ours(args):
             D.read_probe(pool[k % M], sink, stream)
         pe1.record(stream)
     stream.synchronize()
-    read_peak = 3 * probe_bytes / (pe0.elapsed_time(pe1) / 1e3) / 1e9
+    ro_peak = 3 * probe_bytes / (pe0.elapsed_time(pe1) / 1e3) / 1e9
 
     clocks = ClockSampler(dev)
     if ws > 1:
@@ -385,8 +385,8 @@ def run_ours(args):
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config),
             "kernel": kname, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, copy)",
-            "read_only_peak_gbs_this_box": round(read_peak, 1),
-            "frac_of_read_only_peak": round(achieved / read_peak, 4),
+            "read_only_peak_gbs_this_box": round(ro_peak, 1),
+            "frac_of_read_only_peak": round(achieved / ro_peak, 4),
             "frac_of_nominal_8000": round(achieved / 8000.0, 4),
             "avg_launch_ms": round(1e3 * sum(durs) / len(durs), 4),
             "bytes_per_launch": int(sum(byts) / len(byts))}

@@ -121,6 +121,12 @@ struct coadapt_plan {
   uint64_t active = 0;
   std::vector<Range> host;  // ranges, sorted, merged
   Range* ranges = nullptr;  // device copy
+  // TMA chunk numbering per chunk size P: prefix[k] = first chunk of range k
+  struct Chunks {
+    std::vector<uint64_t> prefix;
+    uint64_t* dev = nullptr;
+  };
+  std::vector<std::pair<int, Chunks>> chunks;
 };
 
 struct coadapt_gns {
@@ -297,6 +303,52 @@ int launch_fused_window(coadapt_gns* g, const coadapt_plan* p,
   return COADAPT_OK;
 }
 
+// chunk numbering of `p` for chunk size P (built on first use, synchronous)
+int plan_chunks(coadapt_plan* p, int P, const coadapt_plan::Chunks** out) {
+  for (auto& kv : p->chunks)
+    if (kv.first == P) {
+      *out = &kv.second;
+      return COADAPT_OK;
+    }
+  coadapt_plan::Chunks c;
+  c.prefix.resize(p->host.size() + 1);
+  uint64_t acc = 0;
+  for (size_t k = 0; k < p->host.size(); ++k) {
+    c.prefix[k] = acc;
+    const uint64_t rb = p->host[k].abs_begin, re = rb + p->host[k].len;
+    acc += (re - 1) / P - rb / P + 1;
+  }
+  c.prefix.back() = acc;
+  CU(cudaMalloc(&c.dev, sizeof(uint64_t) * c.prefix.size()));
+  CU(cudaMemcpy(c.dev, c.prefix.data(), sizeof(uint64_t) * c.prefix.size(),
+                cudaMemcpyHostToDevice));
+  p->chunks.emplace_back(P, std::move(c));
+  *out = &p->chunks.back().second;
+  return COADAPT_OK;
+}
+
+bool use_tma_path() {
+  static const char* e = getenv("COADAPT_FUSED_PATH");
+  return !(e && std::string(e) == "ldg");
+}
+
+int launch_fused_tma_all(coadapt_gns* g, coadapt_plan* p, const FusedArgs& fa,
+                         int M, cudaStream_t s) {
+  const int P = coadapt::dev::tma_chunk_elems(p->dtype, M);
+  if (P <= 0) return fail(COADAPT_E_INTERNAL, "no TMA kernel for this dtype/M");
+  const coadapt_plan::Chunks* ch = nullptr;
+  if (int rc = plan_chunks(p, P, &ch)) return rc;
+  const uint64_t nch = ch->prefix.back();
+  if (nch == 0) return COADAPT_OK;
+  const int grid = (int)std::min<uint64_t>(std::max(1, g->sms), nch);
+  if (int rc = ensure_partials(g, (size_t)grid * (M + 1))) return rc;
+  Sink sink{g->partials, g->ticket, g->slots};
+  CU(coadapt::dev::launch_fused_tma(p->dtype, M, p->ranges, (int)p->host.size(),
+                                    ch->dev, 0, nch, fa, sink, grid, s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return COADAPT_OK;
+}
+
 // compacted index of the first active element at or after abs index x
 uint64_t cum_at(const coadapt_plan* p, uint64_t x) {
   const auto& R = p->host;
@@ -370,6 +422,8 @@ int coadapt_plan_destroy(coadapt_plan* p) {
   {
     DeviceGuard guard(p->device);
     if (p->ranges) cudaFree(p->ranges);
+    for (auto& kv : p->chunks)
+      if (kv.second.dev) cudaFree(kv.second.dev);
   }
   delete p;
   return COADAPT_OK;
@@ -546,6 +600,11 @@ int coadapt_gns_fused_sqnorm(coadapt_gns* g, const coadapt_plan* p,
   fa.gslot = g->N;
   fa.gscale = 1.0 / ((double)micro_count * (double)micro_count);
   GUARD(g->device);
+  // TMA bulk copies need 16-byte aligned sources; unaligned bucket views use
+  // the LDG form of the same pass
+  if (use_tma_path() && mod0 == 0)
+    return launch_fused_tma_all(g, const_cast<coadapt_plan*>(p), fa,
+                                micro_count, static_cast<cudaStream_t>(stream));
   return launch_fused_window(g, p, fa, micro_count, Window{0, p->active},
                              static_cast<cudaStream_t>(stream));
 }

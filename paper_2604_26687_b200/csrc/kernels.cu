@@ -23,6 +23,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/coadapt_cuda.h"
 #include "internal.h"
@@ -49,6 +50,12 @@ template <>
 struct Elem<COADAPT_FP64> {
   static constexpr int kSize = 8, kPerVec = 2;
 };
+// bf16 accumulation variants (experiment): 100 = fp32 partial per vector,
+// 101 = per-element F2F + DFMA, 102 = per-element integer bf16->fp64 + DFMA
+constexpr int kBf16F32 = 100, kBf16F2F = 101, kBf16Bits = 102;
+template <> struct Elem<kBf16F32> { static constexpr int kSize = 2, kPerVec = 8; };
+template <> struct Elem<kBf16F2F> { static constexpr int kSize = 2, kPerVec = 8; };
+template <> struct Elem<kBf16Bits> { static constexpr int kSize = 2, kPerVec = 8; };
 
 // Streaming 128-bit load: read-only path, no L1 allocation, 256B L2 prefetch.
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
@@ -99,19 +106,14 @@ __device__ __forceinline__ void unpack<COADAPT_FP32>(const uint4& v,
 // acc += sum of squares of one vector.
 template <int DT>
 __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
-  if constexpr (DT == COADAPT_BF16 || DT == COADAPT_FP16) {
+  if constexpr (DT == kBf16F32) {
     float f[8];
-    unpack<DT>(v, f);
-    // each square is exact in fp32 (<= 22 significant bits); two chains
+    unpack<COADAPT_BF16>(v, f);
     float s0 = f[0] * f[0], s1 = f[1] * f[1];
     s0 = fmaf(f[2], f[2], s0); s1 = fmaf(f[3], f[3], s1);
     s0 = fmaf(f[4], f[4], s0); s1 = fmaf(f[5], f[5], s1);
     s0 = fmaf(f[6], f[6], s0); s1 = fmaf(f[7], f[7], s1);
     const float p = s0 + s1;
-    // fp32 is safe when the partial is finite and >= 2^-100 (subnormal
-    // squares then perturb it by < 2^-47 relative).  Otherwise (|x| near
-    // the fp32-square overflow/underflow limits, Inf/NaN) redo the vector
-    // in fp64; exact zero vectors skip both.
     if (p >= 0x1p-100f && p <= 3.402823466e38f) {
       acc += (double)p;
     } else if (((v.x | v.y | v.z | v.w) & 0x7fff7fffu) != 0u) {
@@ -120,6 +122,45 @@ __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
         const double d = f[i];
         acc = fma(d, d, acc);
       }
+    }
+  } else if constexpr (DT == kBf16F2F || DT == COADAPT_BF16 || DT == COADAPT_FP16) {
+    float f[8];
+    unpack<DT == COADAPT_FP16 ? COADAPT_FP16 : COADAPT_BF16>(v, f);
+    // two fp64 chains per vector halve the dependent DFMA latency
+    double a0 = (double)f[0] * (double)f[0], a1 = (double)f[1] * (double)f[1];
+#pragma unroll
+    for (int i = 2; i < 8; i += 2) {
+      const double d0 = f[i], d1 = f[i + 1];
+      a0 = fma(d0, d0, a0);
+      a1 = fma(d1, d1, a1);
+    }
+    acc += a0 + a1;
+  } else if constexpr (DT == kBf16Bits) {
+    // bf16 -> fp64 without the F2F convert pipe: for a normal bf16 with
+    // magnitude bits h, |x| as a double has high word ((h & 0x7fff) << 13) +
+    // (896 << 20) and a zero low word.  An all-zero vector is skipped (so
+    // zero buckets give exactly 0); a zero or subnormal element inside a
+    // non-zero vector is counted as a magnitude <= 2^-126, whose square
+    // (<= 2^-252) is below half an ulp of any sum >= 2^-199.  Inf/NaN
+    // (exponent 255) map to high words >= 0x47f00000: the vector then
+    // contributes NaN, which finalize reports as a validation error.
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if ((v.x | v.y | v.z | v.w) & 0x7fff7fffu) {
+      uint32_t hw[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        hw[2 * i] = ((w[i] & 0x7fffu) << 13) + 0x38000000u;
+        hw[2 * i + 1] = ((w[i] >> 3) & 0x0fffe000u) + 0x38000000u;
+      }
+      uint32_t mx = hw[0];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) mx = max(mx, hw[i]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double d = __hiloint2double((int)hw[i], 0);
+        acc = fma(d, d, acc);
+      }
+      if (mx >= 0x47f00000u) acc = __longlong_as_double(0x7ff8000000000000ll);
     }
   } else if constexpr (DT == COADAPT_FP32) {
     float f[4];
@@ -139,7 +180,7 @@ __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
 
 template <int DT>
 __device__ __forceinline__ double elem_f64(uintptr_t addr) {
-  if constexpr (DT == COADAPT_BF16) {
+  if constexpr (DT == COADAPT_BF16 || DT >= 100) {
     const uint16_t h = *reinterpret_cast<const uint16_t*>(addr);
     return (double)__uint_as_float((uint32_t)h << 16);
   } else if constexpr (DT == COADAPT_FP16) {
@@ -153,7 +194,7 @@ __device__ __forceinline__ double elem_f64(uintptr_t addr) {
 
 template <int DT>
 __device__ __forceinline__ float elem_f32(uintptr_t addr) {
-  if constexpr (DT == COADAPT_BF16) {
+  if constexpr (DT == COADAPT_BF16 || DT >= 100) {
     const uint16_t h = *reinterpret_cast<const uint16_t*>(addr);
     return __uint_as_float((uint32_t)h << 16);
   } else if constexpr (DT == COADAPT_FP16) {
@@ -263,37 +304,50 @@ __device__ __forceinline__ void piece_sumsq(uintptr_t base, uint64_t a,
   }
   const uint4* __restrict__ vp = reinterpret_cast<const uint4*>(v0);
   const uint64_t nv = (v1 - v0) >> 4;
-  uint64_t i = tid;
-  for (; i + (uint64_t)(U - 1) * NT < nv; i += (uint64_t)U * NT) {
+  // all U loads of an iteration issue back to back (predicated at the end
+  // of the piece), so a misaligned or short piece keeps its MLP
+  for (uint64_t i = tid; i < nv; i += (uint64_t)U * NT) {
     uint4 r[U];
 #pragma unroll
-    for (int j = 0; j < U; ++j) r[j] = ld_stream(vp + i + (uint64_t)j * NT);
+    for (int j = 0; j < U; ++j)
+      r[j] = (i + (uint64_t)j * NT < nv) ? ld_stream(vp + i + (uint64_t)j * NT)
+                                          : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
     for (int j = 0; j < U; ++j) vacc<DT>(r[j], acc);
   }
-  for (; i < nv; i += NT) vacc<DT>(ld_stream(vp + i), acc);
 }
 
 // ---------------------------------------------------------------- K1
 
+// Interleaved chunks: the window of active elements is cut into chunks of
+// U*NT vectors and chunk c goes to CTA c mod G, so all CTAs sweep HBM
+// together (measured 7.35 TB/s read vs 6.5 TB/s for contiguous per-CTA
+// shares, tools/bw_sweep.cu).  The assignment is static, so results stay
+// bit-reproducible.
 template <int DT, int NT, int U>
 __global__ void __launch_bounds__(NT, 4)
     sqnorm_kernel(const Range* __restrict__ R, int nr, Window w,
                   const BatchArgs jobs, Sink sink) {
   __shared__ double red[32];
-  uint64_t e0, e1;
-  cta_share(w, e0, e1);
-  const int k0 = (e0 < e1) ? find_range(R, nr, e0) : nr;
+  constexpr uint64_t CE = (uint64_t)U * NT * (16 / Elem<DT>::kSize);
+  const uint64_t n = w.e_end - w.e_begin;
+  const uint64_t nchunks = (n + CE - 1) / CE;
   for (int b = 0; b < jobs.count; ++b) {
     const uintptr_t base = reinterpret_cast<uintptr_t>(jobs.ptr[b]);
     double total = 0.0;
-    for (int k = k0; k < nr && R[k].cum_begin < e1; ++k) {
-      const uint64_t cb = R[k].cum_begin, ce = cb + R[k].len;
-      const uint64_t s = cb > e0 ? cb : e0, e = ce < e1 ? ce : e1;
-      if (s >= e) continue;
-      double acc = 0.0;
-      piece_sumsq<DT, NT, U>(base, R[k].abs_begin + (s - cb), e - s, acc);
-      total += R[k].weight == 1.0 ? acc : R[k].weight * acc;
+    int k = 0;  // range cursor: chunks of this CTA only move forward
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      const uint64_t e0 = w.e_begin + c * CE;
+      const uint64_t e1 = min(e0 + CE, w.e_end);
+      while (k + 1 < nr && R[k + 1].cum_begin <= e0) ++k;
+      for (int kk = k; kk < nr && R[kk].cum_begin < e1; ++kk) {
+        const uint64_t cb = R[kk].cum_begin, ce = cb + R[kk].len;
+        const uint64_t s = cb > e0 ? cb : e0, e = ce < e1 ? ce : e1;
+        if (s >= e) continue;
+        double acc = 0.0;
+        piece_sumsq<DT, NT, U>(base, R[kk].abs_begin + (s - cb), e - s, acc);
+        total += R[kk].weight == 1.0 ? acc : R[kk].weight * acc;
+      }
     }
     total = block_sum<NT>(total, red);
     if (threadIdx.x == 0)
@@ -439,6 +493,221 @@ __global__ void __launch_bounds__(NT)
     out_scale[threadIdx.x] = threadIdx.x < M ? 1.0 : args.gscale;
   }
   last_cta_combine<NT>(sink, M + 1, out_slot, out_scale, red);
+}
+
+// ---------------------------------------------------------------- K1f (TMA)
+//
+// The B200 form of the fused pass.  Bytes in flight are decoupled from
+// registers: warp 0 (one elected lane) streams each chunk's M tiles into a
+// 3-stage shared-memory ring with cp.async.bulk (TMA, SASS UBLKCP) signalled
+// on an mbarrier; 8 consumer warps square/sum from shared memory and release
+// the stage.  A chunk is the intersection of one range with an absolutely
+// aligned P-element window, so every interior copy is 16-byte aligned and a
+// chunk has one weight; the <16-byte edges of a range are read from global
+// memory directly.  Chunk c goes to CTA c mod G (interleaved sweep).
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
+                                         uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int DT, int M>
+struct TmaCfg {
+  static constexpr int ES = Elem<DT>::kSize;
+  static constexpr int PV = Elem<DT>::kPerVec;
+  static constexpr int kStages = 3;
+  // ~64 KB per stage, tiles a multiple of 256 B (>= 4 KB for M <= 16)
+  static constexpr int kTile = (65536 / M) & ~255;
+  static constexpr int P = kTile / ES;  // elements per chunk
+  static constexpr int kStage = kTile * M;
+  static constexpr int kSmem = kStages * kStage;
+  static constexpr int NT = 288;        // 1 producer + 8 consumer warps
+  static constexpr int CT = NT - 32;
+};
+
+struct ChunkMeta {
+  uint64_t a;   // first element (absolute)
+  uint32_t n;   // elements in the chunk
+  uint32_t pad;
+  double w;     // range weight
+};
+
+template <int DT, int M>
+__device__ __forceinline__ void tma_scalar(const FusedArgs& args, uint64_t i,
+                                           double* acc, double& gacc) {
+  constexpr int ES = Elem<DT>::kSize;
+  float sum = 0.0f;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const float x =
+        elem_f32<DT>(reinterpret_cast<uintptr_t>(args.ptr[m]) + i * ES);
+    const double xd = x;
+    acc[m] = fma(xd, xd, acc[m]);
+    sum = __fadd_rn(sum, x);
+  }
+  const double sd = sum;
+  gacc = fma(sd, sd, gacc);
+}
+
+template <int DT, int M>
+__device__ __forceinline__ void tma_consume(const char* stage,
+                                            const FusedArgs& args,
+                                            const ChunkMeta& cm, int ct,
+                                            double* acc, double& gacc) {
+  using C = TmaCfg<DT, M>;
+  constexpr int VE = 16 / C::ES;
+  const uint64_t a = cm.a, b = cm.a + cm.n;
+  const uint64_t A0 = (a + VE - 1) / VE * VE, A1 = b / VE * VE;
+  if (A1 <= A0) {  // no aligned interior: everything from global
+    for (uint64_t i = a + ct; i < b; i += C::CT) tma_scalar<DT, M>(args, i, acc, gacc);
+    return;
+  }
+  if (a + ct < A0) tma_scalar<DT, M>(args, a + ct, acc, gacc);
+  if (A1 + ct < b) tma_scalar<DT, M>(args, A1 + ct, acc, gacc);
+  const int nv = (int)((A1 - A0) / VE);
+  for (int v = ct; v < nv; v += C::CT) {
+    float sum[C::PV];
+#pragma unroll
+    for (int e = 0; e < C::PV; ++e) sum[e] = 0.0f;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const uint4 x = *reinterpret_cast<const uint4*>(stage + m * C::kTile + v * 16);
+      float f[C::PV];
+      unpack<DT>(x, f);
+      vacc<DT>(x, acc[m]);
+#pragma unroll
+      for (int e = 0; e < C::PV; ++e) sum[e] = __fadd_rn(sum[e], f[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < C::PV; ++e) {
+      const double sd = sum[e];
+      gacc = fma(sd, sd, gacc);
+    }
+  }
+}
+
+template <int DT, int M>
+__global__ void __launch_bounds__(TmaCfg<DT, M>::NT, 1)
+    fused_tma_kernel(const Range* __restrict__ R, int nr,
+                     const uint64_t* __restrict__ prefix, uint64_t c_begin,
+                     uint64_t c_end, const FusedArgs args, Sink sink) {
+  using C = TmaCfg<DT, M>;
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ uint64_t full[C::kStages], empty[C::kStages];
+  __shared__ ChunkMeta meta[C::kStages];
+  __shared__ double red[32];
+  __shared__ int32_t out_slot[M + 1];
+  __shared__ double out_scale[M + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::CT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t G = gridDim.x;
+  double total[M], gtotal = 0.0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) total[m] = 0.0;
+  if (warp == 0) {
+    if (lane == 0) {
+      int k = 0;
+      uint64_t i = 0;
+      for (uint64_t c = c_begin + blockIdx.x; c < c_end; c += G, ++i) {
+        const int st = (int)(i % C::kStages);
+        if (i >= (uint64_t)C::kStages)
+          mbar_wait(&empty[st], (uint32_t)(((i / C::kStages) - 1) & 1));
+        while (k + 1 < nr && prefix[k + 1] <= c) ++k;
+        const uint64_t rb = R[k].abs_begin, re = rb + R[k].len;
+        const uint64_t j = rb / C::P + (c - prefix[k]);
+        const uint64_t a = max(rb, j * C::P), b = min(re, (j + 1) * C::P);
+        meta[st] = ChunkMeta{a, (uint32_t)(b - a), 0u, R[k].weight};
+        constexpr int VE = 16 / C::ES;
+        const uint64_t A0 = (a + VE - 1) / VE * VE, A1 = b / VE * VE;
+        char* dst = smem + st * C::kStage;
+        if (A1 > A0) {
+          const uint32_t bytes = (uint32_t)((A1 - A0) * C::ES);
+          mbar_arrive_tx(&full[st], bytes * M);
+#pragma unroll 1
+          for (int m = 0; m < M; ++m)
+            bulk_g2s(dst + m * C::kTile,
+                     static_cast<const char*>(args.ptr[m]) + A0 * C::ES, bytes,
+                     &full[st]);
+        } else {
+          mbar_arrive(&full[st]);
+        }
+      }
+    }
+  } else {
+    const int ct = threadIdx.x - 32;
+    uint64_t i = 0;
+    for (uint64_t c = c_begin + blockIdx.x; c < c_end; c += G, ++i) {
+      const int st = (int)(i % C::kStages);
+      mbar_wait(&full[st], (uint32_t)((i / C::kStages) & 1));
+      const ChunkMeta cm = meta[st];
+      const char* stage = smem + st * C::kStage;
+      // the tile's first vector is the chunk's first aligned element
+      if (cm.w == 1.0) {
+        tma_consume<DT, M>(stage, args, cm, ct, total, gtotal);
+      } else {
+        double acc[M], g = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = 0.0;
+        tma_consume<DT, M>(stage, args, cm, ct, acc, g);
+#pragma unroll
+        for (int m = 0; m < M; ++m) total[m] += cm.w * acc[m];
+        gtotal += cm.w * g;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const double v = block_sum<C::NT>(total[m], red);
+    if (threadIdx.x == 0) sink.partials[(size_t)m * G + blockIdx.x] = v;
+  }
+  {
+    const double v = block_sum<C::NT>(gtotal, red);
+    if (threadIdx.x == 0) sink.partials[(size_t)M * G + blockIdx.x] = v;
+  }
+  if (threadIdx.x <= M) {
+    out_slot[threadIdx.x] =
+        threadIdx.x < M ? args.slot0 + (int)threadIdx.x : args.gslot;
+    out_scale[threadIdx.x] = threadIdx.x < M ? 1.0 : args.gscale;
+  }
+  last_cta_combine<C::NT>(sink, M + 1, out_slot, out_scale, red);
 }
 
 // ---------------------------------------------------------------- K3
@@ -621,19 +890,16 @@ __global__ void __launch_bounds__(NT)
     read_probe_kernel(const uint4* __restrict__ p, uint64_t nvec,
                       double* sink) {
   uint32_t x = 0;
-  const uint64_t per = (nvec + gridDim.x - 1) / gridDim.x;
-  const uint64_t b = per * blockIdx.x, e = min(nvec, b + per);
-  uint64_t i = b + threadIdx.x;
-  for (; i + (uint64_t)(U - 1) * NT < e; i += (uint64_t)U * NT) {
+  const uint64_t chunk = (uint64_t)U * NT;  // interleaved, as K1
+  for (uint64_t c = blockIdx.x; c * chunk < nvec; c += gridDim.x) {
+    const uint64_t i = c * chunk + threadIdx.x;
     uint4 r[U];
 #pragma unroll
-    for (int j = 0; j < U; ++j) r[j] = ld_stream(p + i + (uint64_t)j * NT);
+    for (int j = 0; j < U; ++j)
+      r[j] = (i + (uint64_t)j * NT < nvec) ? ld_stream(p + i + (uint64_t)j * NT)
+                                            : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
     for (int j = 0; j < U; ++j) x ^= r[j].x ^ r[j].y ^ r[j].z ^ r[j].w;
-  }
-  for (; i < e; i += NT) {
-    const uint4 r = ld_stream(p + i);
-    x ^= r.x ^ r.y ^ r.z ^ r.w;
   }
   if (x == 0x9e3779b9u) *sink = (double)x;  // keeps the loads alive
 }
@@ -683,6 +949,13 @@ void* fused_kernel_ptr(int dtype, int M) {
 }
 
 void* sqnorm_kernel_ptr(int dtype) {
+  if (dtype == COADAPT_BF16) {
+    // experiment hook: COADAPT_BF16_VARIANT=100|101|102
+    static const char* e = getenv("COADAPT_BF16_VARIANT");
+    if (e && atoi(e) == kBf16F32) return sqnorm_fn<kBf16F32>();
+    if (e && atoi(e) == kBf16F2F) return sqnorm_fn<kBf16F2F>();
+    if (e && atoi(e) == kBf16Bits) return sqnorm_fn<kBf16Bits>();
+  }
   switch (dtype) {
     case COADAPT_BF16: return sqnorm_fn<COADAPT_BF16>();
     case COADAPT_FP16: return sqnorm_fn<COADAPT_FP16>();
@@ -700,7 +973,64 @@ int occupancy_of(void* fn, int nt) {
   return occ;
 }
 
+struct TmaFn {
+  void* fn = nullptr;
+  int P = 0, smem = 0, nt = 0;
+};
+
+template <int DT, int M>
+TmaFn tma_fn() {
+  using C = TmaCfg<DT, M>;
+  TmaFn f;
+  f.fn = reinterpret_cast<void*>(&fused_tma_kernel<DT, M>);
+  f.P = C::P;
+  f.smem = C::kSmem;
+  f.nt = C::NT;
+  static bool attr = false;  // opt in to > 48 KB dynamic shared memory once
+  if (!attr) {
+    cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::kSmem);
+    attr = true;
+  }
+  return f;
+}
+
+template <int DT>
+TmaFn tma_fn_rt(int M) {
+  switch (M) {
+#define F(m) \
+  case m:    \
+    return tma_fn<DT, m>();
+    F(1) F(2) F(3) F(4) F(5) F(6) F(7) F(8) F(9) F(10) F(11) F(12) F(13) F(14)
+        F(15) F(16)
+#undef F
+  }
+  return TmaFn{};
+}
+
+TmaFn tma_kernel(int dtype, int M) {
+  switch (dtype) {
+    case COADAPT_BF16: return tma_fn_rt<COADAPT_BF16>(M);
+    case COADAPT_FP16: return tma_fn_rt<COADAPT_FP16>(M);
+    case COADAPT_FP32: return tma_fn_rt<COADAPT_FP32>(M);
+  }
+  return TmaFn{};
+}
+
 }  // namespace
+
+int tma_chunk_elems(int dtype, int M) { return tma_kernel(dtype, M).P; }
+
+cudaError_t launch_fused_tma(int dtype, int M, const Range* ranges, int nranges,
+                             const uint64_t* prefix, uint64_t c_begin,
+                             uint64_t c_end, const FusedArgs& fa, Sink sink,
+                             int grid, cudaStream_t s) {
+  const TmaFn f = tma_kernel(dtype, M);
+  if (!f.fn) return cudaErrorInvalidValue;
+  void* args[] = {(void*)&ranges, (void*)&nranges, (void*)&prefix,
+                  (void*)&c_begin, (void*)&c_end, (void*)&fa, (void*)&sink};
+  return cudaLaunchKernel(f.fn, dim3(grid), dim3(f.nt), args, f.smem, s);
+}
 
 int threads_sqnorm() { return kNT; }
 int threads_fused(int) { return kNTF; }
@@ -776,13 +1106,12 @@ cudaError_t launch_l2_flush(void* buf, uint64_t bytes, cudaStream_t s) {
 
 cudaError_t launch_read_probe(const void* buf, uint64_t bytes, double* sink,
                               cudaStream_t s) {
-  int dev = 0, sms = 148, occ = 0;
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &occ, read_probe_kernel<kNT, kU>, kNT, 0);
-  if (occ < 1) occ = 1;
-  read_probe_kernel<kNT, kU><<<sms * occ, kNT, 0, s>>>(
+  // 4 CTAs x 256 threads x 8 loads per SM: the best LDG point of
+  // tools/bw_sweep.cu (interleaved, 7.35 TB/s)
+  read_probe_kernel<kNT, kU><<<sms * 4, kNT, 0, s>>>(
       static_cast<const uint4*>(buf), bytes / 16, sink);
   return cudaGetLastError();
 }
