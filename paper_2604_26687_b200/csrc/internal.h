@@ -67,7 +67,7 @@ cudaError_t launch_fused_tma(int dtype, int M, const Range* ranges, int nranges,
 // max resident CTAs per SM for the kernel that launch_* would pick
 int occupancy_sqnorm(int dtype);
 int occupancy_fused(int dtype, int M);
-int threads_sqnorm();
+int threads_sqnorm(int dtype);
 int threads_fused(int M);
 
 struct FinalizeArgs {

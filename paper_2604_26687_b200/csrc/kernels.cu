@@ -52,7 +52,8 @@ struct Elem<COADAPT_FP64> {
 };
 // bf16 accumulation variants (experiment): 100 = fp32 partial per vector,
 // 101 = per-element F2F + DFMA, 102 = per-element integer bf16->fp64 + DFMA
-constexpr int kBf16F32 = 100, kBf16F2F = 101, kBf16Bits = 102;
+constexpr int kBf16F32 = 100, kBf16F2F = 101, kBf16Bits = 102, kBf16Hybrid = 103;
+template <> struct Elem<kBf16Hybrid> { static constexpr int kSize = 2, kPerVec = 8; };
 template <> struct Elem<kBf16F32> { static constexpr int kSize = 2, kPerVec = 8; };
 template <> struct Elem<kBf16F2F> { static constexpr int kSize = 2, kPerVec = 8; };
 template <> struct Elem<kBf16Bits> { static constexpr int kSize = 2, kPerVec = 8; };
@@ -135,6 +136,30 @@ __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
       a1 = fma(d1, d1, a1);
     }
     acc += a0 + a1;
+  } else if constexpr (DT == kBf16Hybrid) {
+    // Balance the convert (XU) and integer (ALU) pipes: the low bf16 of each
+    // 32-bit word goes through F2F; the high bf16's |x| is built as an fp64
+    // directly (high word ((w & 0x7fff0000) >> 3) + (896 << 20), low word
+    // 0), exact for normal values.  A zero/subnormal high element counts as
+    // |x| <= 2^-126 (square <= 2^-252, below half an ulp of any sum >= 2^-199);
+    // all-zero vectors are skipped, so zero buckets give exactly 0.  An
+    // Inf/NaN high element (high word >= 0x47f00000) poisons the vector.
+    if ((v.x | v.y | v.z | v.w) & 0x7fff7fffu) {
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      double a0 = 0.0, a1 = 0.0;
+      uint32_t mx = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double lo = (double)__uint_as_float(w[i] << 16);
+        const uint32_t hw = ((w[i] & 0x7fff0000u) >> 3) + 0x38000000u;
+        mx = max(mx, hw);
+        const double hi = __hiloint2double((int)hw, 0);
+        a0 = fma(lo, lo, a0);
+        a1 = fma(hi, hi, a1);
+      }
+      acc += a0 + a1;
+      if (mx >= 0x47f00000u) acc = __longlong_as_double(0x7ff8000000000000ll);
+    }
   } else if constexpr (DT == kBf16Bits) {
     // bf16 -> fp64 without the F2F convert pipe: for a normal bf16 with
     // magnitude bits h, |x| as a double has high word ((h & 0x7fff) << 13) +
@@ -304,8 +329,17 @@ __device__ __forceinline__ void piece_sumsq(uintptr_t base, uint64_t a,
   }
   const uint4* __restrict__ vp = reinterpret_cast<const uint4*>(v0);
   const uint64_t nv = (v1 - v0) >> 4;
-  // all U loads of an iteration issue back to back (predicated at the end
-  // of the piece), so a misaligned or short piece keeps its MLP
+  if (nv == (uint64_t)U * NT) {
+    // a full aligned chunk (the common case): U unguarded loads in flight
+    uint4 r[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) r[j] = ld_stream(vp + tid + j * NT);
+#pragma unroll
+    for (int j = 0; j < U; ++j) vacc<DT>(r[j], acc);
+    return;
+  }
+  // partial / misaligned piece: all U loads of an iteration still issue
+  // back to back (predicated), so the piece keeps its MLP
   for (uint64_t i = tid; i < nv; i += (uint64_t)U * NT) {
     uint4 r[U];
 #pragma unroll
@@ -324,8 +358,8 @@ __device__ __forceinline__ void piece_sumsq(uintptr_t base, uint64_t a,
 // together (measured 7.35 TB/s read vs 6.5 TB/s for contiguous per-CTA
 // shares, tools/bw_sweep.cu).  The assignment is static, so results stay
 // bit-reproducible.
-template <int DT, int NT, int U>
-__global__ void __launch_bounds__(NT, 4)
+template <int DT, int NT, int U, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
     sqnorm_kernel(const Range* __restrict__ R, int nr, Window w,
                   const BatchArgs jobs, Sink sink) {
   __shared__ double red[32];
@@ -602,7 +636,7 @@ __device__ __forceinline__ void tma_consume(const char* stage,
     for (int m = 0; m < M; ++m) {
       const uint4 x = *reinterpret_cast<const uint4*>(stage + m * C::kTile + v * 16);
       float f[C::PV];
-      unpack<DT>(x, f);
+      unpack<(DT >= 100 ? COADAPT_BF16 : DT)>(x, f);
       vacc<DT>(x, acc[m]);
 #pragma unroll
       for (int e = 0; e < C::PV; ++e) sum[e] = __fadd_rn(sum[e], f[e]);
@@ -916,9 +950,14 @@ struct FusedCfg {
   static constexpr int UP = M >= 8 ? 1 : (M >= 4 ? 2 : (M >= 2 ? 4 : 8));
 };
 
-template <int DT>
-void* sqnorm_fn() {
-  return reinterpret_cast<void*>(&sqnorm_kernel<DT, kNT, kU>);
+struct K1Fn {
+  void* fn = nullptr;
+  int nt = 0;
+};
+
+template <int DT, int NT = kNT, int U = kU, int MINB = 4>
+K1Fn sqnorm_fn() {
+  return K1Fn{reinterpret_cast<void*>(&sqnorm_kernel<DT, NT, U, MINB>), NT};
 }
 
 template <int DT, int M>
@@ -948,13 +987,26 @@ void* fused_kernel_ptr(int dtype, int M) {
   return nullptr;
 }
 
-void* sqnorm_kernel_ptr(int dtype) {
+K1Fn sqnorm_kernel_ptr(int dtype) {
   if (dtype == COADAPT_BF16) {
-    // experiment hook: COADAPT_BF16_VARIANT=100|101|102
+    // experiment hooks: COADAPT_BF16_VARIANT=100..103, COADAPT_K1_CFG=0..4
     static const char* e = getenv("COADAPT_BF16_VARIANT");
     if (e && atoi(e) == kBf16F32) return sqnorm_fn<kBf16F32>();
     if (e && atoi(e) == kBf16F2F) return sqnorm_fn<kBf16F2F>();
     if (e && atoi(e) == kBf16Bits) return sqnorm_fn<kBf16Bits>();
+    if (e && atoi(e) == kBf16Hybrid) return sqnorm_fn<kBf16Hybrid>();
+    static const char* c = getenv("COADAPT_K1_CFG");
+    switch (c ? atoi(c) : 0) {
+      case 1: return sqnorm_fn<COADAPT_BF16, 256, 4, 6>();
+      case 2: return sqnorm_fn<COADAPT_BF16, 512, 4, 3>();
+      case 3: return sqnorm_fn<COADAPT_BF16, 128, 8, 8>();
+      case 4: return sqnorm_fn<COADAPT_BF16, 256, 6, 5>();
+      case 5: return sqnorm_fn<COADAPT_BF16, 256, 2, 8>();
+      case 6: return sqnorm_fn<COADAPT_BF16, 256, 8, 3>();
+      case 7: return sqnorm_fn<COADAPT_BF16, 256, 16, 2>();
+      case 8: return sqnorm_fn<COADAPT_BF16, 128, 8, 6>();
+      default: break;
+    }
   }
   switch (dtype) {
     case COADAPT_BF16: return sqnorm_fn<COADAPT_BF16>();
@@ -962,7 +1014,7 @@ void* sqnorm_kernel_ptr(int dtype) {
     case COADAPT_FP32: return sqnorm_fn<COADAPT_FP32>();
     case COADAPT_FP64: return sqnorm_fn<COADAPT_FP64>();
   }
-  return nullptr;
+  return K1Fn{};
 }
 
 int occupancy_of(void* fn, int nt) {
@@ -1009,6 +1061,11 @@ TmaFn tma_fn_rt(int M) {
 }
 
 TmaFn tma_kernel(int dtype, int M) {
+  if (dtype == COADAPT_BF16) {
+    static const char* e = getenv("COADAPT_BF16_VARIANT");
+    if (e && atoi(e) == kBf16Hybrid) return tma_fn_rt<kBf16Hybrid>(M);
+    if (e && atoi(e) == kBf16F32) return tma_fn_rt<kBf16F32>(M);
+  }
   switch (dtype) {
     case COADAPT_BF16: return tma_fn_rt<COADAPT_BF16>(M);
     case COADAPT_FP16: return tma_fn_rt<COADAPT_FP16>(M);
@@ -1032,10 +1089,11 @@ cudaError_t launch_fused_tma(int dtype, int M, const Range* ranges, int nranges,
   return cudaLaunchKernel(f.fn, dim3(grid), dim3(f.nt), args, f.smem, s);
 }
 
-int threads_sqnorm() { return kNT; }
+int threads_sqnorm(int dtype) { return sqnorm_kernel_ptr(dtype).nt; }
 int threads_fused(int) { return kNTF; }
 int occupancy_sqnorm(int dtype) {
-  return occupancy_of(sqnorm_kernel_ptr(dtype), kNT);
+  const K1Fn f = sqnorm_kernel_ptr(dtype);
+  return occupancy_of(f.fn, f.nt);
 }
 int occupancy_fused(int dtype, int M) {
   return occupancy_of(fused_kernel_ptr(dtype, M), kNTF);
@@ -1044,11 +1102,11 @@ int occupancy_fused(int dtype, int M) {
 cudaError_t launch_sqnorm_batched(int dtype, const Range* ranges, int nranges,
                                   Window w, const BatchArgs& jobs, Sink sink,
                                   int grid, cudaStream_t s) {
-  void* fn = sqnorm_kernel_ptr(dtype);
-  if (!fn) return cudaErrorInvalidValue;
+  const K1Fn f = sqnorm_kernel_ptr(dtype);
+  if (!f.fn) return cudaErrorInvalidValue;
   void* args[] = {(void*)&ranges, (void*)&nranges, (void*)&w, (void*)&jobs,
                   (void*)&sink};
-  return cudaLaunchKernel(fn, dim3(grid), dim3(kNT), args, 0, s);
+  return cudaLaunchKernel(f.fn, dim3(grid), dim3(f.nt), args, 0, s);
 }
 
 cudaError_t launch_fused(int dtype, int M, const Range* ranges, int nranges,
