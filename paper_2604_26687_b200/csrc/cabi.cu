@@ -327,6 +327,21 @@ int plan_chunks(coadapt_plan* p, int P, const coadapt_plan::Chunks** out) {
   return COADAPT_OK;
 }
 
+// number of chunks (size P) that start before absolute element x, x a
+// multiple of P: per range, its chunks j with j*P < x
+uint64_t chunks_before(const coadapt_plan* p, const coadapt_plan::Chunks* ch,
+                       int P, uint64_t x) {
+  uint64_t n = 0;
+  for (size_t k = 0; k < p->host.size(); ++k) {
+    const uint64_t rb = p->host[k].abs_begin, re = rb + p->host[k].len;
+    const uint64_t j0 = rb / P, j1 = (re - 1) / P + 1;  // chunks [j0, j1)
+    const uint64_t jx = x / P;
+    if (jx <= j0) break;
+    n = ch->prefix[k] + (std::min(jx, j1) - j0);
+  }
+  return n;
+}
+
 bool use_tma_path() {
   static const char* e = getenv("COADAPT_FUSED_PATH");
   return !(e && std::string(e) == "ldg");
@@ -662,12 +677,19 @@ int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
   // the compute stream must be done with every stage before we overwrite it
   for (int i = 0; i < kStages; ++i) CU(cudaEventRecord(g->stage_free[i], s));
   const uint64_t numel = p->bucket_numel;
-  const uint64_t nchunks = (numel + kStageElems - 1) / kStageElems;
-  for (uint64_t c = 0; c < nchunks; ++c) {
-    const uint64_t w0 = c * kStageElems;
-    const uint64_t w1 = std::min(numel, w0 + kStageElems);
-    const Window win{cum_at(p, w0), cum_at(p, w1)};
-    if (win.e_end == win.e_begin) continue;  // chunk holds only weight-0 data
+  // windows are whole multiples of the TMA chunk size P, so every window is
+  // a contiguous run of the plan's chunk numbering
+  const int P = coadapt::dev::tma_chunk_elems(p->dtype, micro_count);
+  if (P <= 0) return fail(COADAPT_E_INTERNAL, "no TMA kernel for this dtype/M");
+  const coadapt_plan::Chunks* ch = nullptr;
+  if (int rc = plan_chunks(const_cast<coadapt_plan*>(p), P, &ch)) return rc;
+  const uint64_t win = (kStageElems / P) * P;
+  const uint64_t nwin = (numel + win - 1) / win;
+  for (uint64_t c = 0; c < nwin; ++c) {
+    const uint64_t w0 = c * win;
+    const uint64_t w1 = std::min(numel, w0 + win);
+    const uint64_t cb = chunks_before(p, ch, P, w0), ce = chunks_before(p, ch, P, w1);
+    if (ce == cb) continue;  // window holds only weight-0 data
     const int st = (int)(c % kStages);
     char* stage = static_cast<char*>(g->staging) +
                   (size_t)st * coadapt::dev::kMaxFusedM * stage_stride;
@@ -688,7 +710,13 @@ int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
     fa.slot0 = 0;
     fa.gslot = g->N;
     fa.gscale = 1.0 / ((double)micro_count * (double)micro_count);
-    if (int rc = launch_fused_window(g, p, fa, micro_count, win, s)) return rc;
+    const int grid = (int)std::min<uint64_t>(std::max(1, g->sms), ce - cb);
+    if (int rc = ensure_partials(g, (size_t)grid * (micro_count + 1))) return rc;
+    Sink sink{g->partials, g->ticket, g->slots};
+    CU(coadapt::dev::launch_fused_tma(p->dtype, micro_count, p->ranges,
+                                      (int)p->host.size(), ch->dev, cb, ce, fa,
+                                      sink, grid, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     CU(cudaEventRecord(g->stage_free[st], s));
   }
   return COADAPT_OK;

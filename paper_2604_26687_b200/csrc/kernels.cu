@@ -50,14 +50,6 @@ template <>
 struct Elem<COADAPT_FP64> {
   static constexpr int kSize = 8, kPerVec = 2;
 };
-// bf16 accumulation variants (experiment): 100 = fp32 partial per vector,
-// 101 = per-element F2F + DFMA, 102 = per-element integer bf16->fp64 + DFMA
-constexpr int kBf16F32 = 100, kBf16F2F = 101, kBf16Bits = 102, kBf16Hybrid = 103;
-template <> struct Elem<kBf16Hybrid> { static constexpr int kSize = 2, kPerVec = 8; };
-template <> struct Elem<kBf16F32> { static constexpr int kSize = 2, kPerVec = 8; };
-template <> struct Elem<kBf16F2F> { static constexpr int kSize = 2, kPerVec = 8; };
-template <> struct Elem<kBf16Bits> { static constexpr int kSize = 2, kPerVec = 8; };
-
 // Streaming 128-bit load: read-only path, no L1 allocation, 256B L2 prefetch.
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
@@ -104,29 +96,18 @@ __device__ __forceinline__ void unpack<COADAPT_FP32>(const uint4& v,
   f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
 }
 
-// acc += sum of squares of one vector.
+// acc += sum of squares of one vector, every square exact in fp64.
+// bf16/fp16 -> fp32 is exact and free (a shift); fp32 -> fp64 is one F2F on
+// the XU pipe, which is what bounds these kernels at ~6.6 TB/s (1.97 GHz).
+// Cheaper variants were measured and rejected: an fp32
+// partial per vector is +5% faster but biased by ~-6e-9 relative (rounding
+// of structured bf16 squares); integer-built fp64 moves the bound to the
+// ALU/issue pipes and is slower.
 template <int DT>
 __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
-  if constexpr (DT == kBf16F32) {
+  if constexpr (DT == COADAPT_BF16 || DT == COADAPT_FP16) {
     float f[8];
-    unpack<COADAPT_BF16>(v, f);
-    float s0 = f[0] * f[0], s1 = f[1] * f[1];
-    s0 = fmaf(f[2], f[2], s0); s1 = fmaf(f[3], f[3], s1);
-    s0 = fmaf(f[4], f[4], s0); s1 = fmaf(f[5], f[5], s1);
-    s0 = fmaf(f[6], f[6], s0); s1 = fmaf(f[7], f[7], s1);
-    const float p = s0 + s1;
-    if (p >= 0x1p-100f && p <= 3.402823466e38f) {
-      acc += (double)p;
-    } else if (((v.x | v.y | v.z | v.w) & 0x7fff7fffu) != 0u) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double d = f[i];
-        acc = fma(d, d, acc);
-      }
-    }
-  } else if constexpr (DT == kBf16F2F || DT == COADAPT_BF16 || DT == COADAPT_FP16) {
-    float f[8];
-    unpack<DT == COADAPT_FP16 ? COADAPT_FP16 : COADAPT_BF16>(v, f);
+    unpack<DT>(v, f);
     // two fp64 chains per vector halve the dependent DFMA latency
     double a0 = (double)f[0] * (double)f[0], a1 = (double)f[1] * (double)f[1];
 #pragma unroll
@@ -136,57 +117,6 @@ __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
       a1 = fma(d1, d1, a1);
     }
     acc += a0 + a1;
-  } else if constexpr (DT == kBf16Hybrid) {
-    // Balance the convert (XU) and integer (ALU) pipes: the low bf16 of each
-    // 32-bit word goes through F2F; the high bf16's |x| is built as an fp64
-    // directly (high word ((w & 0x7fff0000) >> 3) + (896 << 20), low word
-    // 0), exact for normal values.  A zero/subnormal high element counts as
-    // |x| <= 2^-126 (square <= 2^-252, below half an ulp of any sum >= 2^-199);
-    // all-zero vectors are skipped, so zero buckets give exactly 0.  An
-    // Inf/NaN high element (high word >= 0x47f00000) poisons the vector.
-    if ((v.x | v.y | v.z | v.w) & 0x7fff7fffu) {
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-      double a0 = 0.0, a1 = 0.0;
-      uint32_t mx = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double lo = (double)__uint_as_float(w[i] << 16);
-        const uint32_t hw = ((w[i] & 0x7fff0000u) >> 3) + 0x38000000u;
-        mx = max(mx, hw);
-        const double hi = __hiloint2double((int)hw, 0);
-        a0 = fma(lo, lo, a0);
-        a1 = fma(hi, hi, a1);
-      }
-      acc += a0 + a1;
-      if (mx >= 0x47f00000u) acc = __longlong_as_double(0x7ff8000000000000ll);
-    }
-  } else if constexpr (DT == kBf16Bits) {
-    // bf16 -> fp64 without the F2F convert pipe: for a normal bf16 with
-    // magnitude bits h, |x| as a double has high word ((h & 0x7fff) << 13) +
-    // (896 << 20) and a zero low word.  An all-zero vector is skipped (so
-    // zero buckets give exactly 0); a zero or subnormal element inside a
-    // non-zero vector is counted as a magnitude <= 2^-126, whose square
-    // (<= 2^-252) is below half an ulp of any sum >= 2^-199.  Inf/NaN
-    // (exponent 255) map to high words >= 0x47f00000: the vector then
-    // contributes NaN, which finalize reports as a validation error.
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    if ((v.x | v.y | v.z | v.w) & 0x7fff7fffu) {
-      uint32_t hw[8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        hw[2 * i] = ((w[i] & 0x7fffu) << 13) + 0x38000000u;
-        hw[2 * i + 1] = ((w[i] >> 3) & 0x0fffe000u) + 0x38000000u;
-      }
-      uint32_t mx = hw[0];
-#pragma unroll
-      for (int i = 1; i < 8; ++i) mx = max(mx, hw[i]);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double d = __hiloint2double((int)hw[i], 0);
-        acc = fma(d, d, acc);
-      }
-      if (mx >= 0x47f00000u) acc = __longlong_as_double(0x7ff8000000000000ll);
-    }
   } else if constexpr (DT == COADAPT_FP32) {
     float f[4];
     unpack<DT>(v, f);
@@ -205,7 +135,7 @@ __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
 
 template <int DT>
 __device__ __forceinline__ double elem_f64(uintptr_t addr) {
-  if constexpr (DT == COADAPT_BF16 || DT >= 100) {
+  if constexpr (DT == COADAPT_BF16) {
     const uint16_t h = *reinterpret_cast<const uint16_t*>(addr);
     return (double)__uint_as_float((uint32_t)h << 16);
   } else if constexpr (DT == COADAPT_FP16) {
@@ -219,7 +149,7 @@ __device__ __forceinline__ double elem_f64(uintptr_t addr) {
 
 template <int DT>
 __device__ __forceinline__ float elem_f32(uintptr_t addr) {
-  if constexpr (DT == COADAPT_BF16 || DT >= 100) {
+  if constexpr (DT == COADAPT_BF16) {
     const uint16_t h = *reinterpret_cast<const uint16_t*>(addr);
     return __uint_as_float((uint32_t)h << 16);
   } else if constexpr (DT == COADAPT_FP16) {
@@ -584,8 +514,9 @@ struct TmaCfg {
   static constexpr int P = kTile / ES;  // elements per chunk
   static constexpr int kStage = kTile * M;
   static constexpr int kSmem = kStages * kStage;
-  static constexpr int NT = 288;        // 1 producer + 8 consumer warps
-  static constexpr int CT = NT - 32;
+  static constexpr int NW = 16;         // consumer warps
+  static constexpr int CT = NW * 32;
+  static constexpr int NT = CT + 32;    // + 1 producer warp
 };
 
 struct ChunkMeta {
@@ -595,40 +526,34 @@ struct ChunkMeta {
   double w;     // range weight
 };
 
-template <int DT, int M>
-__device__ __forceinline__ void tma_scalar(const FusedArgs& args, uint64_t i,
-                                           double* acc, double& gacc) {
-  constexpr int ES = Elem<DT>::kSize;
-  float sum = 0.0f;
-#pragma unroll
-  for (int m = 0; m < M; ++m) {
-    const float x =
-        elem_f32<DT>(reinterpret_cast<uintptr_t>(args.ptr[m]) + i * ES);
-    const double xd = x;
-    acc[m] = fma(xd, xd, acc[m]);
-    sum = __fadd_rn(sum, x);
-  }
-  const double sd = sum;
-  gacc = fma(sd, sd, gacc);
+// Element i (absolute) of micro-bucket m, as fp32 (edges of a chunk).
+template <int DT>
+__device__ __forceinline__ float elem_at(const FusedArgs& args, int m,
+                                         uint64_t i) {
+  return elem_f32<DT>(reinterpret_cast<uintptr_t>(args.ptr[m]) +
+                      i * Elem<DT>::kSize);
 }
 
-template <int DT, int M>
-__device__ __forceinline__ void tma_consume(const char* stage,
-                                            const FusedArgs& args,
-                                            const ChunkMeta& cm, int ct,
-                                            double* acc, double& gacc) {
+// One chunk, one consumer group (GT threads): each thread owns whole
+// positions (16-byte columns across the M tiles): acc[m] += x_m^2 in fp64
+// and the M values of each element are summed in micro-batch order in fp32
+// (Megatron main_grad order), the sum squared in fp64.  The <16-byte edges
+// of a range come from global memory.
+template <int DT, int M, int GT, bool WEIGHTED>
+__device__ __forceinline__ void tma_consume_cols(const char* stage,
+                                                 const FusedArgs& args,
+                                                 const ChunkMeta& cm, int gt,
+                                                 double* acc, double& gacc) {
   using C = TmaCfg<DT, M>;
   constexpr int VE = 16 / C::ES;
+  constexpr int UP = DT;
   const uint64_t a = cm.a, b = cm.a + cm.n;
-  const uint64_t A0 = (a + VE - 1) / VE * VE, A1 = b / VE * VE;
-  if (A1 <= A0) {  // no aligned interior: everything from global
-    for (uint64_t i = a + ct; i < b; i += C::CT) tma_scalar<DT, M>(args, i, acc, gacc);
-    return;
-  }
-  if (a + ct < A0) tma_scalar<DT, M>(args, a + ct, acc, gacc);
-  if (A1 + ct < b) tma_scalar<DT, M>(args, A1 + ct, acc, gacc);
+  uint64_t A0 = (a + VE - 1) / VE * VE, A1 = b / VE * VE;
+  if (A1 <= A0) A0 = A1 = b;  // no aligned interior
+  const int nhead = (int)(A0 - a), ntail = (int)(b - A1);
   const int nv = (int)((A1 - A0) / VE);
-  for (int v = ct; v < nv; v += C::CT) {
+  const double w = cm.w;
+  for (int v = gt; v < nv; v += GT) {
     float sum[C::PV];
 #pragma unroll
     for (int e = 0; e < C::PV; ++e) sum[e] = 0.0f;
@@ -636,16 +561,37 @@ __device__ __forceinline__ void tma_consume(const char* stage,
     for (int m = 0; m < M; ++m) {
       const uint4 x = *reinterpret_cast<const uint4*>(stage + m * C::kTile + v * 16);
       float f[C::PV];
-      unpack<(DT >= 100 ? COADAPT_BF16 : DT)>(x, f);
-      vacc<DT>(x, acc[m]);
+      unpack<UP>(x, f);
+      if constexpr (WEIGHTED) {
+        double t = 0.0;
+        vacc<DT>(x, t);
+        acc[m] = fma(w, t, acc[m]);
+      } else {
+        vacc<DT>(x, acc[m]);
+      }
 #pragma unroll
       for (int e = 0; e < C::PV; ++e) sum[e] = __fadd_rn(sum[e], f[e]);
     }
+    double g = 0.0;
 #pragma unroll
     for (int e = 0; e < C::PV; ++e) {
       const double sd = sum[e];
-      gacc = fma(sd, sd, gacc);
+      g = fma(sd, sd, g);
     }
+    gacc = WEIGHTED ? fma(w, g, gacc) : gacc + g;
+  }
+  for (int q = gt; q < nhead + ntail; q += GT) {
+    const uint64_t i = q < nhead ? a + q : A1 + (q - nhead);
+    float sum = 0.0f;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const float x = elem_at<DT>(args, m, i);
+      const double xd = x;
+      acc[m] = fma(WEIGHTED ? w * xd : xd, xd, acc[m]);
+      sum = __fadd_rn(sum, x);
+    }
+    const double sd = sum;
+    gacc = fma(WEIGHTED ? w * sd : sd, sd, gacc);
   }
 }
 
@@ -654,7 +600,11 @@ __global__ void __launch_bounds__(TmaCfg<DT, M>::NT, 1)
     fused_tma_kernel(const Range* __restrict__ R, int nr,
                      const uint64_t* __restrict__ prefix, uint64_t c_begin,
                      uint64_t c_end, const FusedArgs args, Sink sink) {
+  // Two consumer groups of NW/2 warps take alternate chunks; every thread
+  // owns whole positions of a chunk (tma_consume_cols), so per-thread state
+  // is M fp64 accumulators and nothing is read twice from shared memory.
   using C = TmaCfg<DT, M>;
+  constexpr int GW = C::NW / 2;  // warps per chunk
   extern __shared__ __align__(1024) char smem[];
   __shared__ uint64_t full[C::kStages], empty[C::kStages];
   __shared__ ChunkMeta meta[C::kStages];
@@ -665,15 +615,16 @@ __global__ void __launch_bounds__(TmaCfg<DT, M>::NT, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::CT / 32);
+      mbar_init(&empty[s], GW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const uint64_t G = gridDim.x;
-  double total[M], gtotal = 0.0;
+  double acc[M];
 #pragma unroll
-  for (int m = 0; m < M; ++m) total[m] = 0.0;
+  for (int m = 0; m < M; ++m) acc[m] = 0.0;
+  double gtotal = 0.0;
   if (warp == 0) {
     if (lane == 0) {
       int k = 0;
@@ -704,32 +655,26 @@ __global__ void __launch_bounds__(TmaCfg<DT, M>::NT, 1)
       }
     }
   } else {
-    const int ct = threadIdx.x - 32;
-    uint64_t i = 0;
-    for (uint64_t c = c_begin + blockIdx.x; c < c_end; c += G, ++i) {
+    const int grp = (warp - 1) / GW;
+    const int gt = ((warp - 1) % GW) * 32 + lane;
+    uint64_t i = grp;
+    for (uint64_t c = c_begin + blockIdx.x + grp * G; c < c_end; c += 2 * G, i += 2) {
       const int st = (int)(i % C::kStages);
       mbar_wait(&full[st], (uint32_t)((i / C::kStages) & 1));
       const ChunkMeta cm = meta[st];
-      const char* stage = smem + st * C::kStage;
-      // the tile's first vector is the chunk's first aligned element
-      if (cm.w == 1.0) {
-        tma_consume<DT, M>(stage, args, cm, ct, total, gtotal);
-      } else {
-        double acc[M], g = 0.0;
-#pragma unroll
-        for (int m = 0; m < M; ++m) acc[m] = 0.0;
-        tma_consume<DT, M>(stage, args, cm, ct, acc, g);
-#pragma unroll
-        for (int m = 0; m < M; ++m) total[m] += cm.w * acc[m];
-        gtotal += cm.w * g;
-      }
+      if (cm.w == 1.0)
+        tma_consume_cols<DT, M, GW * 32, false>(smem + st * C::kStage, args, cm,
+                                                gt, acc, gtotal);
+      else
+        tma_consume_cols<DT, M, GW * 32, true>(smem + st * C::kStage, args, cm,
+                                               gt, acc, gtotal);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
 #pragma unroll
   for (int m = 0; m < M; ++m) {
-    const double v = block_sum<C::NT>(total[m], red);
+    const double v = block_sum<C::NT>(acc[m], red);
     if (threadIdx.x == 0) sink.partials[(size_t)m * G + blockIdx.x] = v;
   }
   {
@@ -988,26 +933,6 @@ void* fused_kernel_ptr(int dtype, int M) {
 }
 
 K1Fn sqnorm_kernel_ptr(int dtype) {
-  if (dtype == COADAPT_BF16) {
-    // experiment hooks: COADAPT_BF16_VARIANT=100..103, COADAPT_K1_CFG=0..4
-    static const char* e = getenv("COADAPT_BF16_VARIANT");
-    if (e && atoi(e) == kBf16F32) return sqnorm_fn<kBf16F32>();
-    if (e && atoi(e) == kBf16F2F) return sqnorm_fn<kBf16F2F>();
-    if (e && atoi(e) == kBf16Bits) return sqnorm_fn<kBf16Bits>();
-    if (e && atoi(e) == kBf16Hybrid) return sqnorm_fn<kBf16Hybrid>();
-    static const char* c = getenv("COADAPT_K1_CFG");
-    switch (c ? atoi(c) : 0) {
-      case 1: return sqnorm_fn<COADAPT_BF16, 256, 4, 6>();
-      case 2: return sqnorm_fn<COADAPT_BF16, 512, 4, 3>();
-      case 3: return sqnorm_fn<COADAPT_BF16, 128, 8, 8>();
-      case 4: return sqnorm_fn<COADAPT_BF16, 256, 6, 5>();
-      case 5: return sqnorm_fn<COADAPT_BF16, 256, 2, 8>();
-      case 6: return sqnorm_fn<COADAPT_BF16, 256, 8, 3>();
-      case 7: return sqnorm_fn<COADAPT_BF16, 256, 16, 2>();
-      case 8: return sqnorm_fn<COADAPT_BF16, 128, 8, 6>();
-      default: break;
-    }
-  }
   switch (dtype) {
     case COADAPT_BF16: return sqnorm_fn<COADAPT_BF16>();
     case COADAPT_FP16: return sqnorm_fn<COADAPT_FP16>();
@@ -1061,11 +986,6 @@ TmaFn tma_fn_rt(int M) {
 }
 
 TmaFn tma_kernel(int dtype, int M) {
-  if (dtype == COADAPT_BF16) {
-    static const char* e = getenv("COADAPT_BF16_VARIANT");
-    if (e && atoi(e) == kBf16Hybrid) return tma_fn_rt<kBf16Hybrid>(M);
-    if (e && atoi(e) == kBf16F32) return tma_fn_rt<kBf16F32>(M);
-  }
   switch (dtype) {
     case COADAPT_BF16: return tma_fn_rt<COADAPT_BF16>(M);
     case COADAPT_FP16: return tma_fn_rt<COADAPT_FP16>(M);

@@ -179,14 +179,15 @@ def test_argument_validation(D, L):
 
 # ---------------------------------------------------------------- K1f
 
+@pytest.mark.parametrize("off", [0, 1])  # 0: TMA bulk-copy path, 1: unaligned LDG path
 @pytest.mark.parametrize("dtype", [0, 1, 2])
 @pytest.mark.parametrize("M", [1, 2, 3, 4, 8, 16])
-def test_fused_matches_oracle(D, L, dtype, M):
+def test_fused_matches_oracle(D, L, dtype, M, off):
     numel = 200_003
     segs = [(0, 70_001, 1.0), (70_001, 4096, 0.0), (74_097, numel - 74_097, 1.0)]
     gen = [(0, numel, 0, numel, numel)]
     unit = O.noise_unit_for(2 ** -10, 1024.0, 1)
-    bufs = [_dev_buf(D, numel, dtype, gen, 77, m, unit, offset_elems=1)[1] for m in range(M)]
+    bufs = [_dev_buf(D, numel, dtype, gen, 77, m, unit, offset_elems=off)[1] for m in range(M)]
     plan = D.BucketPlan(segs, numel, dtype, 0)
     g = D.GnsDevice(1, max(M, 2), max(M, 2), 0) if M >= 2 else None
     if M == 1:
@@ -203,9 +204,11 @@ def test_fused_matches_oracle(D, L, dtype, M):
     assert _rel(parts[M], ss / (M * M)) <= RTOL_NORM
 
 
-def test_fused_host_streaming_matches_device(D, L):
-    M, numel = 4, (16 << 20) + 12_345  # spans two 16 Mi-element staging chunks
-    segs = [(0, 1000, 1.0), (1000, 5000, 0.0), (6000, numel - 6000, 1.0)]
+@pytest.mark.parametrize("M", [3, 4])
+def test_fused_host_streaming_matches_device(D, L, M):
+    numel = (16 << 20) + 12_345  # spans two staging windows
+    segs = [(0, 1000, 1.0), (1000, 5000, 0.0), (6000, 8_000_000, 1.0),
+            (8_006_000, 3, 0.5), (8_006_003, numel - 8_006_003, 1.0)]
     gen = [(0, numel, 3, numel, numel)]
     unit = O.noise_unit_for(2 ** -10, 256.0, 1)
     bufs = [_dev_buf(D, numel, L.BF16, gen, 5, m, unit)[1] for m in range(M)]
@@ -219,6 +222,9 @@ def test_fused_host_streaming_matches_device(D, L):
     g.fused_sqnorm_host(plan, host)
     b = g.partials()
     assert np.allclose(a, b, rtol=1e-12, atol=0)
+    s, ss = O.fused_sqnorms([_host_u(x) for x in bufs], O.BF16, segs, 8)
+    assert np.allclose(a[:M], s, rtol=RTOL_NORM, atol=0)
+    assert _rel(a[-1], ss / (M * M)) <= RTOL_NORM
 
 
 # ---------------------------------------------------------------- K2 + K3

@@ -17,9 +17,32 @@ from paper_2604_26687_b200 import _lib as L  # noqa: E402
 from paper_2604_26687_b200 import device as D  # noqa: E402
 
 
+SUSTAIN = [0.0]
+
+
 def timed(fn, reps, stream):
     fn()
     torch.cuda.synchronize()
+    if SUSTAIN[0] > 0:
+        # run for SUSTAIN seconds; time only the second half (steady state)
+        import time
+        t0 = time.time()
+        while time.time() - t0 < SUSTAIN[0] / 2:
+            for _ in range(5):
+                fn()
+            torch.cuda.synchronize()
+        n = 0
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        t1 = time.time()
+        while time.time() - t1 < SUSTAIN[0] / 2:
+            for _ in range(5):
+                fn()
+            n += 5
+            torch.cuda.synchronize()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n / 1e3
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(reps):
@@ -36,7 +59,10 @@ def main():
     ap.add_argument("--fused-m", type=int, default=16)
     ap.add_argument("--fused-gb", type=float, default=16.0)
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--sustain", type=float, default=0.0,
+                    help="seconds of back-to-back launches per kernel (power-cap steady state)")
     args = ap.parse_args()
+    SUSTAIN[0] = args.sustain
     torch.cuda.set_device(0)
     s = torch.cuda.Stream()
     dt = {"bf16": L.BF16, "fp32": L.FP32, "fp16": L.FP16}[args.dtype]
