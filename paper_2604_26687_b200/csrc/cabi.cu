@@ -327,15 +327,15 @@ int plan_chunks(coadapt_plan* p, int P, const coadapt_plan::Chunks** out) {
   return COADAPT_OK;
 }
 
-// number of chunks (size P) that start before absolute element x, x a
-// multiple of P: per range, its chunks j with j*P < x
+// number of chunks (size P) that start before absolute element x (x is a
+// multiple of P, or the bucket end): per range, its chunks j with j*P < x
 uint64_t chunks_before(const coadapt_plan* p, const coadapt_plan::Chunks* ch,
                        int P, uint64_t x) {
   uint64_t n = 0;
+  const uint64_t jx = (x + P - 1) / P;
   for (size_t k = 0; k < p->host.size(); ++k) {
     const uint64_t rb = p->host[k].abs_begin, re = rb + p->host[k].len;
     const uint64_t j0 = rb / P, j1 = (re - 1) / P + 1;  // chunks [j0, j1)
-    const uint64_t jx = x / P;
     if (jx <= j0) break;
     n = ch->prefix[k] + (std::min(jx, j1) - j0);
   }

@@ -1,0 +1,97 @@
+"""Multi-GPU worker (launched with torch.distributed.run, one process per GPU).
+
+Each physical rank reduces the buckets of its block of the job's d*t*p
+virtual ranks into its GnsDevice slots, the library's NCCL communicator
+all-reduces the N+1 scalars, and every rank finalizes.  Rank 0 then
+recomputes the whole job alone on its GPU (no NCCL) and checks that the
+all-reduced slots and the step result agree.  Prints one JSON line on rank 0.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2604_26687_b200 import _lib as L  # noqa: E402
+from paper_2604_26687_b200 import device as D  # noqa: E402
+from paper_2604_26687_b200 import dist as Dist  # noqa: E402
+from paper_2604_26687_b200 import layout as Lay  # noqa: E402
+
+
+def run_job(g, lays, ranks, M, d, seed, unit, fused):
+    g.begin_step()
+    for vr in ranks:
+        lay = lays[vr]
+        i_d = lay.coords[0]
+        plan = D.BucketPlan(lay.segments, lay.numel, L.BF16, torch.cuda.current_device())
+        bufs = []
+        for m in range(M):
+            b = torch.empty(lay.numel, dtype=torch.bfloat16, device="cuda")
+            D.synth_fill(b, lay.gen, seed, i_d * M + m, Lay.G0, unit)
+            bufs.append(b)
+        if fused:
+            g.fused_sqnorm(plan, bufs)
+        else:
+            g.micro_sqnorm_batched(plan, bufs, [i_d] * M, list(range(M)))
+            mean = torch.empty(lay.numel, dtype=torch.bfloat16, device="cuda")
+            D.synth_mean_fill(mean, lay.gen, seed, 0, d * M, Lay.G0, unit)
+            sl = D.BucketPlan(lay.segments, lay.numel, L.BF16, torch.cuda.current_device(),
+                              slice_index=i_d, slice_count=d)
+            g.mean_sqnorm(sl, mean)
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    spec = Lay.tiny_model(layers=4, h=128, ffn=256, vocab=512, tied=True)
+    unit = Lay.noise_unit_for(256.0, 1)
+    report = {"world": world, "cases": []}
+    ok = True
+    for (d, t, p, M, fused) in [(2, 2, 2, 4, False), (1, 4, 2, 4, True), (8, 1, 1, 2, False)]:
+        R = d * t * p
+        lays = Lay.world_layouts(spec, d, t, p)
+        mine = Dist.block_map(R, world, rank)
+        g = D.GnsDevice(d, M, d * M, local)
+        Dist.attach(g, dist, world, rank)
+        run_job(g, lays, mine, M, d, 0xC0905, unit, fused)
+        g.allreduce()
+        g.finalize(d * M * 2048)
+        r = g.result()
+        parts = g.partials()
+        dist.barrier()
+        case = {"dtp": [d, t, p], "M": M, "fused": fused}
+        if rank == 0:
+            ref = D.GnsDevice(d, M, d * M, local)
+            run_job(ref, lays, list(range(R)), M, d, 0xC0905, unit, fused)
+            ref.finalize(d * M * 2048)
+            rr = ref.result()
+            rp = ref.partials()
+            rel = float(np.max(np.abs(parts - rp) / np.maximum(np.abs(rp), 1e-300)))
+            case.update({"max_rel_slots": rel, "phi": r.phi, "phi_ref": rr.phi,
+                         "b_simple_rel": abs(r.b_simple - rr.b_simple) / abs(rr.b_simple)})
+            ok = ok and rel <= 1e-12 and case["b_simple_rel"] <= 1e-10
+        # every rank finalized the same all-reduced slots
+        t_phi = torch.tensor([r.phi], dtype=torch.float64, device="cuda")
+        lo, hi = t_phi.clone(), t_phi.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        case["phi_identical_on_all_ranks"] = bool(lo.item() == hi.item())
+        ok = ok and case["phi_identical_on_all_ranks"]
+        report["cases"].append(case)
+        g.close()
+    report["ok"] = bool(ok)
+    if rank == 0:
+        print(json.dumps(report), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
