@@ -1,0 +1,58 @@
+"""The C++ boundary is a drop-in: tests/cpp/dropin_main.cpp, written against
+the reference's public headers, compiles and links against
+libcoadapt_b200.so with this repo's include/coadapt/ and — when the
+reference is mounted (build container only) — with the reference's own
+headers (proj/include/coadapt/, plus the <string> include gns.hpp forgot,
+SURVEY §0 item 6)."""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIBDIR = os.path.join(ROOT, "paper_2604_26687_b200", "lib")
+REF_INC = "/root/reference/proj/include"
+CXX = shutil.which("g++", path="/usr/bin") or shutil.which("g++")
+
+
+def _build(include_dir, out, extra=()):
+    cmd = [CXX, "-std=c++20", "-O1", *extra, "-I", include_dir,
+           os.path.join(HERE, "cpp", "dropin_main.cpp"), "-L", LIBDIR, "-lcoadapt_b200",
+           f"-Wl,-rpath,{LIBDIR}", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
+def _run(exe, *args):
+    env = dict(os.environ)
+    # the library's NEEDED libnccl.so.2 resolves to the system copy here
+    r = subprocess.run([exe, *args], capture_output=True, text=True, env=env, timeout=300)
+    return r
+
+
+@pytest.fixture(scope="module")
+def exe_ours(tmp_path_factory):
+    out = str(tmp_path_factory.mktemp("dropin") / "dropin_ours")
+    _build(os.path.join(ROOT, "include"), out)
+    return out
+
+
+def test_ours_headers_build_and_pass(exe_ours):
+    r = _run(exe_ours)
+    assert r.returncode == 0 and r.stdout.strip().startswith("OK"), r.stdout + r.stderr
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers not mounted")
+def test_reference_headers_link_against_our_library(tmp_path):
+    out = str(tmp_path / "dropin_ref")
+    _build(REF_INC, out, extra=("-include", "string"))
+    r = _run(out)
+    assert r.returncode == 0 and r.stdout.strip().startswith("OK"), r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_span_overload_on_device(exe_ours):
+    r = _run(exe_ours, "--gpu")
+    assert r.returncode == 0 and r.stdout.strip().startswith("OK"), r.stdout + r.stderr
