@@ -186,6 +186,24 @@ int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* plan,
                                   const void* const* host_buckets,
                                   int micro_count, void* stream);
 
+/* Trainer form.  The gradient-accumulation add a trainer
+ * does anyway — Megatron's fp32 main_grad.add_(grad) — with the GNS norms
+ * fused in, over the WHOLE bucket (every element is accumulated; only
+ * weight != 0 elements are counted):
+ *   main_grad = (flags & FIRST) ? grad : main_grad + grad      (fp32, RN)
+ *   s_{dp_index, micro} += sum w * grad^2                         (fp64)
+ *   (flags & LAST_MEAN, d == 1): gbar^2 += mean_scale_sq * sum w * main_grad^2
+ * so the estimate costs no HBM bytes beyond the accumulation's own.  Both
+ * buffers 16-byte aligned; main_grad fp32, grad of the plan's dtype.
+ * Replaces: the backward-hook norm of the paper's GNS manager
+ * feeding record_micro_batch (gns.hpp:19-20). */
+#define COADAPT_ACC_FIRST 1
+#define COADAPT_ACC_LAST_MEAN 2
+int coadapt_gns_accumulate(coadapt_gns* g, const coadapt_plan* plan,
+                           float* main_grad, const void* micro_grad,
+                           int dp_index, int micro, int flags,
+                           double mean_scale_sq, void* stream);
+
 /* NCCL over NVLink: sum the N+1 slots over all ranks (Alg. 1 AllReduce,
  * PAPER.md:443; the reference models it as summation). */
 int coadapt_nccl_unique_id(void* out, size_t len); /* len >= 128 */

@@ -127,6 +127,7 @@ SIGNATURES = {
     "coadapt_gns_fused_sqnorm": (I, [P, P, P, I, P]),
     "coadapt_gns_mean_sqnorm": (I, [P, P, P, P]),
     "coadapt_gns_fused_sqnorm_host": (I, [P, P, P, I, P]),
+    "coadapt_gns_accumulate": (I, [P, P, P, P, I, I, I, D, P]),
     "coadapt_nccl_unique_id": (I, [P, SZ]),
     "coadapt_gns_attach_nccl": (I, [P, I, I, P, SZ]),
     "coadapt_gns_allreduce": (I, [P, P]),

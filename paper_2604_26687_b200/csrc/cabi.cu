@@ -127,6 +127,12 @@ struct coadapt_plan {
     uint64_t* dev = nullptr;
   };
   std::vector<std::pair<int, Chunks>> chunks;
+  // whole-bucket table for the trainer form (weight-0 ranges and gaps
+  // included, abs == cum); built lazily, not for DP-slice plans
+  bool is_slice = false;
+  std::vector<Range> full_host;
+  Range* full = nullptr;
+  std::vector<coadapt_segment> segs;  // as given (sorted)
 };
 
 struct coadapt_gns {
@@ -228,6 +234,12 @@ int plan_make(const coadapt_segment* segs, size_t nseg, uint64_t bucket_numel,
     delete p;
     return rc;
   }
+  p->is_slice = !(lo == 0 && hi == bucket_numel);
+  p->segs.assign(segs, segs + nseg);
+  std::stable_sort(p->segs.begin(), p->segs.end(),
+                   [](const coadapt_segment& a, const coadapt_segment& b) {
+                     return a.offset < b.offset;
+                   });
   if (!p->host.empty()) {
     cudaError_t e = cudaMalloc(&p->ranges, sizeof(Range) * p->host.size());
     if (e == cudaSuccess)
@@ -342,6 +354,30 @@ uint64_t chunks_before(const coadapt_plan* p, const coadapt_plan::Chunks* ch,
   return n;
 }
 
+// whole-bucket range table (every element exactly once; gaps weight 0)
+int plan_full(coadapt_plan* p) {
+  if (p->full || p->bucket_numel == 0) return COADAPT_OK;
+  std::vector<Range>& f = p->full_host;
+  uint64_t at = 0;
+  auto push = [&](uint64_t b, uint64_t n, double w) {
+    if (n == 0) return;
+    if (!f.empty() && f.back().weight == w && f.back().abs_begin + f.back().len == b)
+      f.back().len += n;
+    else
+      f.push_back(Range{b, b, n, w});
+  };
+  for (const auto& s : p->segs) {
+    if (s.offset > at) push(at, s.offset - at, 0.0);
+    push(s.offset, s.numel, s.weight);
+    at = s.offset + s.numel;
+  }
+  if (at < p->bucket_numel) push(at, p->bucket_numel - at, 0.0);
+  CU(cudaMalloc(&p->full, sizeof(Range) * f.size()));
+  CU(cudaMemcpy(p->full, f.data(), sizeof(Range) * f.size(),
+                cudaMemcpyHostToDevice));
+  return COADAPT_OK;
+}
+
 bool use_tma_path() {
   static const char* e = getenv("COADAPT_FUSED_PATH");
   return !(e && std::string(e) == "ldg");
@@ -437,6 +473,7 @@ int coadapt_plan_destroy(coadapt_plan* p) {
   {
     DeviceGuard guard(p->device);
     if (p->ranges) cudaFree(p->ranges);
+    if (p->full) cudaFree(p->full);
     for (auto& kv : p->chunks)
       if (kv.second.dev) cudaFree(kv.second.dev);
   }
@@ -719,6 +756,49 @@ int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
     g_launches.fetch_add(1, std::memory_order_relaxed);
     CU(cudaEventRecord(g->stage_free[st], s));
   }
+  return COADAPT_OK;
+}
+
+int coadapt_gns_accumulate(coadapt_gns* g, const coadapt_plan* p,
+                           float* main_grad, const void* micro_grad,
+                           int dp_index, int micro, int flags,
+                           double mean_scale_sq, void* stream) {
+  if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
+  if (p->device != g->device)
+    return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
+  if (p->is_slice)
+    return fail(COADAPT_E_VALIDATION, "accumulate needs a whole-bucket plan");
+  if (p->dtype == COADAPT_FP64)
+    return fail(COADAPT_E_VALIDATION, "fp64 gradients are not supported here");
+  if (flags & ~(COADAPT_ACC_FIRST | COADAPT_ACC_LAST_MEAN))
+    return fail(COADAPT_E_VALIDATION, "unknown accumulate flags");
+  if ((flags & COADAPT_ACC_LAST_MEAN) && g->dp != 1)
+    return fail(COADAPT_E_VALIDATION,
+                "LAST_MEAN needs d == 1 (the local sum is the mean gradient); "
+                "for d > 1 reduce the synchronised gradient with mean_sqnorm");
+  if (!(mean_scale_sq >= 0.0) || !std::isfinite(mean_scale_sq))
+    return fail(COADAPT_E_VALIDATION, "mean_scale_sq must be finite and >= 0");
+  if (int rc = check_slot(g, dp_index, micro)) return rc;
+  if (p->bucket_numel && (!main_grad || !micro_grad))
+    return fail(COADAPT_E_VALIDATION, "main_grad/micro_grad is NULL");
+  if ((reinterpret_cast<uintptr_t>(main_grad) & 15) ||
+      (reinterpret_cast<uintptr_t>(micro_grad) & 15))
+    return fail(COADAPT_E_VALIDATION,
+                "main_grad and micro_grad must be 16-byte aligned");
+  GUARD(g->device);
+  coadapt_plan* pm = const_cast<coadapt_plan*>(p);
+  if (int rc = plan_full(pm)) return rc;
+  if (p->bucket_numel == 0) return COADAPT_OK;
+  const int grid = grid_for(g->device, coadapt::dev::occupancy_accum(p->dtype),
+                            p->bucket_numel);
+  if (int rc = ensure_partials(g, (size_t)grid * 2)) return rc;
+  Sink sink{g->partials, g->ticket, g->slots};
+  coadapt::dev::AccumArgs a{main_grad, micro_grad, flags,
+                            dp_index * g->M + micro, g->N, mean_scale_sq};
+  CU(coadapt::dev::launch_accum(p->dtype, p->full, (int)p->full_host.size(),
+                                p->bucket_numel, a, sink, grid,
+                                static_cast<cudaStream_t>(stream)));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return COADAPT_OK;
 }
 

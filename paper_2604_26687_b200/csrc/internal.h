@@ -70,6 +70,19 @@ int occupancy_fused(int dtype, int M);
 int threads_sqnorm(int dtype);
 int threads_fused(int M);
 
+// Trainer form: main_grad (+)= grad over the whole bucket, s += w*grad^2
+// (slot), and with flags&2 gbar^2 += gscale*w*main_grad^2 (gslot).
+struct AccumArgs {
+  float* main_grad;
+  const void* grad;
+  int flags;  // 1: first micro-batch (main_grad = grad), 2: also gbar^2
+  int32_t slot, gslot;
+  double gscale;
+};
+int occupancy_accum(int dtype);
+cudaError_t launch_accum(int dtype, const Range* full, int nfull, uint64_t numel,
+                         const AccumArgs& a, Sink sink, int grid, cudaStream_t s);
+
 struct FinalizeArgs {
   const double* slots;
   int32_t n;               // N; slots[N] = gbar^2

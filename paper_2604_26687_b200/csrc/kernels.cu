@@ -689,6 +689,142 @@ __global__ void __launch_bounds__(TmaCfg<DT, M>::NT, 1)
   last_cta_combine<C::NT>(sink, M + 1, out_slot, out_scale, red);
 }
 
+// ---------------------------------------------------------------- KA
+//
+// Trainer form: the gradient-accumulation add a trainer
+// performs anyway (Megatron: main_grad.add_(grad), fp32) with s_m fused in,
+// and, on the last micro-batch of a d = 1 step, gbar^2 from the updated
+// main_grad.  The norm then costs no HBM bytes beyond the accumulation's
+// own (read g, read+write main_grad).  The table covers the WHOLE bucket
+// (weight-0 ranges and gaps included): every element is accumulated, only
+// weighted ones are counted.
+
+__device__ __forceinline__ uint4 ld_rw(const uint4* p) {  // main_grad: read+write
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <int DT>
+__device__ __forceinline__ void accum_elem(float* mg, float g, double w,
+                                           bool first, bool mean, double& s,
+                                           double& gm) {
+  const float nv = first ? g : __fadd_rn(*mg, g);
+  *mg = nv;
+  if (w != 0.0) {
+    const double gd = g, nd = nv;
+    s = fma(w * gd, gd, s);
+    if (mean) gm = fma(w * nd, nd, gm);
+  }
+}
+
+template <int DT, int NT, int U>
+__global__ void __launch_bounds__(NT, 3)
+    accum_kernel(const Range* __restrict__ R, int nr, uint64_t numel,
+                 float* __restrict__ mg, const void* __restrict__ gp, int flags,
+                 int32_t slot, int32_t gslot, double gscale, Sink sink) {
+  static_assert(DT == COADAPT_BF16 || DT == COADAPT_FP16 || DT == COADAPT_FP32, "");
+  constexpr int ES = Elem<DT>::kSize, PV = Elem<DT>::kPerVec;
+  constexpr uint64_t CE = (uint64_t)U * NT * PV;  // elements per chunk
+  __shared__ double red[32];
+  const bool first = flags & 1, mean = flags & 2;
+  const uint64_t nchunks = (numel + CE - 1) / CE;
+  double s = 0.0, gm = 0.0;
+  int k = 0;
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint64_t e0 = c * CE, e1 = min(e0 + CE, numel);
+    while (k + 1 < nr && R[k + 1].abs_begin <= e0) ++k;
+    for (int kk = k; kk < nr && R[kk].abs_begin < e1; ++kk) {
+      const uint64_t a = max(R[kk].abs_begin, e0);
+      const uint64_t b = min(R[kk].abs_begin + R[kk].len, e1);
+      if (a >= b) continue;
+      const double w = R[kk].weight;
+      // vectors of PV elements aligned on the element index (both buffers are
+      // 16-byte aligned, checked by the host), edges element by element
+      const uint64_t A0 = (a + PV - 1) / PV * PV, A1 = b / PV * PV;
+      const char* gb = static_cast<const char*>(gp);
+      if (A1 <= A0) {
+        for (uint64_t i = a + threadIdx.x; i < b; i += NT)
+          accum_elem<DT>(mg + i, elem_f32<DT>(reinterpret_cast<uintptr_t>(gb + i * ES)),
+                         w, first, mean, s, gm);
+        continue;
+      }
+      if (a + threadIdx.x < A0) {
+        const uint64_t i = a + threadIdx.x;
+        accum_elem<DT>(mg + i, elem_f32<DT>(reinterpret_cast<uintptr_t>(gb + i * ES)), w,
+                       first, mean, s, gm);
+      }
+      if (A1 + threadIdx.x < b) {
+        const uint64_t i = A1 + threadIdx.x;
+        accum_elem<DT>(mg + i, elem_f32<DT>(reinterpret_cast<uintptr_t>(gb + i * ES)), w,
+                       first, mean, s, gm);
+      }
+      const uint64_t nv = (A1 - A0) / PV;
+      const uint4* gv = reinterpret_cast<const uint4*>(gb + A0 * ES);
+      uint4* mv = reinterpret_cast<uint4*>(mg + A0);  // PV floats = PV/4 uint4
+      for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)U * NT) {
+        uint4 gr[U], mr[U][PV / 4];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const uint64_t v = v0 + (uint64_t)j * NT;
+          if (v < nv) {
+            gr[j] = ld_stream(gv + v);
+#pragma unroll
+            for (int h = 0; h < PV / 4; ++h)
+              mr[j][h] = first ? make_uint4(0u, 0u, 0u, 0u) : ld_rw(mv + v * (PV / 4) + h);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const uint64_t v = v0 + (uint64_t)j * NT;
+          if (v >= nv) continue;
+          float f[PV];
+          unpack<DT>(gr[j], f);
+          float* mf = reinterpret_cast<float*>(mr[j]);
+          double a0 = 0.0, a1 = 0.0, m0 = 0.0, m1 = 0.0;
+#pragma unroll
+          for (int e = 0; e < PV; ++e) {
+            const float nvf = first ? f[e] : __fadd_rn(mf[e], f[e]);
+            mf[e] = nvf;
+            const double gd = f[e];
+            if (e & 1) a1 = fma(gd, gd, a1); else a0 = fma(gd, gd, a0);
+            if (mean) {
+              const double nd = nvf;
+              if (e & 1) m1 = fma(nd, nd, m1); else m0 = fma(nd, nd, m0);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < PV / 4; ++h) st_stream(mv + v * (PV / 4) + h, mr[j][h]);
+          if (w != 0.0) {
+            s = fma(w, a0 + a1, s);
+            if (mean) gm = fma(w, m0 + m1, gm);
+          }
+        }
+      }
+    }
+  }
+  const double vs = block_sum<NT>(s, red);
+  if (threadIdx.x == 0) sink.partials[blockIdx.x] = vs;
+  const double vg = block_sum<NT>(gm, red);
+  if (threadIdx.x == 0) sink.partials[gridDim.x + blockIdx.x] = vg;
+  __shared__ int32_t out_slot[2];
+  __shared__ double out_scale[2];
+  if (threadIdx.x == 0) {
+    out_slot[0] = slot;
+    out_slot[1] = gslot;
+    out_scale[0] = 1.0;
+    out_scale[1] = gscale;
+  }
+  last_cta_combine<NT>(sink, mean ? 2 : 1, out_slot, out_scale, red);
+}
+
 // ---------------------------------------------------------------- K3
 
 struct DevState {  // == coadapt_gns_state
@@ -1037,6 +1173,36 @@ cudaError_t launch_fused(int dtype, int M, const Range* ranges, int nranges,
   void* args[] = {(void*)&ranges, (void*)&nranges, (void*)&w, (void*)&fa,
                   (void*)&sink};
   return cudaLaunchKernel(fn, dim3(grid), dim3(kNTF), args, 0, s);
+}
+
+namespace {
+constexpr int kNTA = 256, kUA = 4;
+void* accum_fn(int dtype) {
+  switch (dtype) {
+    case COADAPT_BF16: return reinterpret_cast<void*>(&accum_kernel<COADAPT_BF16, kNTA, kUA>);
+    case COADAPT_FP16: return reinterpret_cast<void*>(&accum_kernel<COADAPT_FP16, kNTA, kUA>);
+    case COADAPT_FP32: return reinterpret_cast<void*>(&accum_kernel<COADAPT_FP32, kNTA, kUA>);
+  }
+  return nullptr;
+}
+}  // namespace
+
+int occupancy_accum(int dtype) { return occupancy_of(accum_fn(dtype), kNTA); }
+
+cudaError_t launch_accum(int dtype, const Range* full, int nfull, uint64_t numel,
+                         const AccumArgs& a, Sink sink, int grid,
+                         cudaStream_t s) {
+  void* fn = accum_fn(dtype);
+  if (!fn) return cudaErrorInvalidValue;
+  float* mg = a.main_grad;
+  const void* g = a.grad;
+  int flags = a.flags;
+  int32_t slot = a.slot, gslot = a.gslot;
+  double gscale = a.gscale;
+  void* args[] = {(void*)&full, (void*)&nfull, (void*)&numel, (void*)&mg,
+                  (void*)&g,    (void*)&flags, (void*)&slot,  (void*)&gslot,
+                  (void*)&gscale, (void*)&sink};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(kNTA), args, 0, s);
 }
 
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t s) {

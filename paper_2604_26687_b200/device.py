@@ -141,6 +141,22 @@ class GnsDevice:
                                           for b in host_buckets])
         check(lib().coadapt_gns_fused_sqnorm_host(self.handle, plan.handle, ptrs, k, _stream(stream)))
 
+    ACC_FIRST, ACC_LAST_MEAN = 1, 2
+
+    def accumulate(self, plan: BucketPlan, main_grad: torch.Tensor, micro_grad, dp_index: int,
+                   micro: int, first: bool = False, last_mean: bool = False,
+                   mean_scale_sq: Optional[float] = None, stream=None) -> None:
+        """Trainer form: main_grad (+)= micro_grad (fp32) with s_m (and, on the
+        last micro-batch of a d == 1 step, gbar^2) fused in."""
+        if main_grad.dtype != torch.float32:
+            raise L.ValidationError("main_grad must be fp32")
+        flags = (self.ACC_FIRST if first else 0) | (self.ACC_LAST_MEAN if last_mean else 0)
+        if mean_scale_sq is None:
+            mean_scale_sq = 1.0 / float(self.micro_count) ** 2
+        check(lib().coadapt_gns_accumulate(self.handle, plan.handle, main_grad.data_ptr(),
+                                           _ptr(micro_grad), int(dp_index), int(micro), flags,
+                                           float(mean_scale_sq), _stream(stream)))
+
     def mean_sqnorm(self, plan: BucketPlan, mean_grad, stream=None) -> None:
         check(lib().coadapt_gns_mean_sqnorm(self.handle, plan.handle, _ptr(mean_grad), _stream(stream)))
 

@@ -397,3 +397,58 @@ def test_full_size_3b_bucket_against_oracle(D, L, Lay):
     import os
     ref = O.sqnorm_mt(host, O.BF16, lay.segments, os.cpu_count() or 1)
     assert _rel(got, ref) <= RTOL_NORM, (got, ref)
+
+
+# ---------------------------------------------------------------- KA (trainer form)
+
+@pytest.mark.parametrize("dtype", [0, 2])
+def test_accumulate_fused_into_grad_accumulation(D, L, dtype):
+    M, numel = 4, 300_017
+    # weighted segments with a weight-0 (TP duplicate) hole and an uncovered gap
+    segs = [(0, 100_000, 1.0), (100_000, 4_096, 0.0), (104_096, 50_000, 1.0),
+            (160_000, numel - 160_000, 1.0)]
+    gen = [(0, numel, 0, numel, numel)]
+    unit = O.noise_unit_for(2 ** -10, 256.0, 1)
+    tdt = getattr(torch, TDT[dtype])
+    grads = []
+    for m in range(M):
+        b = torch.empty(numel, dtype=tdt, device="cuda")
+        D.synth_fill(b, gen, 21, m, 2 ** -10, unit)
+        grads.append(b)
+    plan = D.BucketPlan(segs, numel, dtype, 0)
+    g = D.GnsDevice(1, M, M, 0)
+    main = torch.full((numel,), 123.0, dtype=torch.float32, device="cuda")  # stale
+    g.begin_step()
+    for m in range(M):
+        g.accumulate(plan, main, grads[m], 0, m, first=(m == 0), last_mean=(m == M - 1))
+    parts = g.partials()
+    # main_grad is exactly torch's sequential fp32 accumulation
+    ref = grads[0].float().clone()
+    for m in range(1, M):
+        ref.add_(grads[m].float())
+    assert torch.equal(main, ref)
+    host = [_host_u(b) for b in grads]
+    s, ss = O.fused_sqnorms(host, dtype, segs, 4)
+    for m in range(M):
+        assert _rel(parts[m], s[m]) <= RTOL_NORM
+    assert _rel(parts[M], ss / (M * M)) <= RTOL_NORM
+    # the same numbers as the pure GNS pass
+    g2 = D.GnsDevice(1, M, M, 0)
+    g2.begin_step()
+    g2.fused_sqnorm(plan, grads)
+    assert np.allclose(parts, g2.partials(), rtol=1e-12, atol=0)
+
+
+def test_accumulate_validation(D, L):
+    n = 1024
+    plan = D.BucketPlan([(0, n, 1.0)], n, L.BF16, 0)
+    sl = D.BucketPlan([(0, n, 1.0)], n, L.BF16, 0, slice_index=0, slice_count=2)
+    g = D.GnsDevice(2, 2, 4, 0)
+    main = torch.zeros(n + 4, dtype=torch.float32, device="cuda")
+    grad = torch.zeros(n, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(L.ValidationError):
+        g.accumulate(plan, main, grad, 0, 0, last_mean=True)  # d > 1
+    with pytest.raises(L.ValidationError):
+        g.accumulate(sl, main, grad, 0, 0)  # slice plan
+    with pytest.raises(L.ValidationError):
+        g.accumulate(plan, main[1:], grad, 0, 0)  # misaligned main_grad

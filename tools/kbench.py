@@ -91,6 +91,17 @@ def main():
         sec = timed(lambda: g.fused_sqnorm(fplan, bufs, s), args.reps, s)
         out["k1f_gbs"] = round(nb * M * es / sec / 1e9, 1)
         out["k1f_bytes"] = nb * M * es
+        # trainer form: fp32 main_grad += grad with s_m fused, vs torch's add_
+        na = nb
+        main = torch.zeros(na, dtype=torch.float32, device="cuda")
+        aplan = D.BucketPlan([(0, na, 1.0)], na, dt, 0)
+        acc_bytes = na * (es + 8)  # read grad, read + write main_grad
+        sec = timed(lambda: g.accumulate(aplan, main, bufs[1], 0, 1, stream=s), args.reps, s)
+        out["accum_fused_gbs"] = round(acc_bytes / sec / 1e9, 1)
+        out["accum_fused_ms"] = round(sec * 1e3, 3)
+        sec_t = timed(lambda: main.add_(bufs[1]), args.reps, s)
+        out["accum_torch_ms"] = round(sec_t * 1e3, 3)
+        out["accum_torch_gbs"] = round(acc_bytes / sec_t / 1e9, 1)
     print(json.dumps(out), flush=True)
 
 
