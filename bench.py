@@ -312,7 +312,9 @@ def run_ours(args):
     local_bytes = sum(l.counted for l in mine) * M * es
     if not fused:
         local_bytes += sum(pl.active_elements for pl in slices) * es
-    launch_bytes = [pl.active_elements * es * (M if fused else 1) for pl in plans]
+    # one launch per virtual rank covers its M micro-buckets (fused pass, or
+    # the batched K1 over the M buckets)
+    launch_bytes = [pl.active_elements * es * M for pl in plans]
 
     ev_pairs = []
 
