@@ -3,22 +3,21 @@
 //   K1  sqnorm_kernel  : s += sum_ranges w * ||bucket[range]||^2 for a batch
 //                        of buckets sharing one layout, and
 //                        the d > 1 mean-gradient read.
-//   K1f fused_kernel   : d = 1: all M micro-buckets of a rank in one pass,
-//                        every s_m plus ||sum_m g_m||^2 (no second read).
+//   K1f fused_tma_kernel: d = 1: all M micro-buckets of a rank in one pass
+//                        (TMA bulk ring), every s_m plus ||sum_m g_m||^2;
+//                        fused_kernel is its LDG form for unaligned buckets.
+//   KA  accum_kernel   : trainer form, fp32 grad accumulation + s_m (+ gbar^2).
 //   K3  finalize_kernel: finalize_step + update_ema + gns (gns.hpp:42-73).
 //   K0  synth kernels  : integer-exact synthetic gradients (test/bench data).
 //
-// Bandwidth design (B200, HBM3e): the reductions are pure streams.  Each CTA
-// owns one contiguous, equal share of the bucket's active elements (perfect
-// byte balance, DRAM-page friendly), walks it with 128-bit
-// ld.global.nc.L1::no_allocate loads, U independent loads in flight per
-// thread, and several CTAs per SM, so that ~100+ KB per SM is in flight
-// (Little's law at ~7 TB/s x ~1 us needs ~45 KB/SM).  Weight-0 ranges (TP
-// duplicates) are never loaded.  Squares of bf16/fp16 are exact in fp32;
-// each 16-byte vector's 8 squares are summed in fp32 and promoted once to
-// the thread's fp64 accumulator; fp32/fp64 inputs square in fp64.  CTA
-// partials are combined by the last CTA in a fixed order, so results are
-// bit-reproducible run to run.
+// Bandwidth design (B200, HBM3e): the reductions are pure streams.  The
+// active elements are cut into chunks assigned CTA c <- chunk c mod G, so
+// all CTAs sweep HBM together (7.35 TB/s read ceiling measured by
+// tools/bw_sweep.cu, vs ~6.5 TB/s for contiguous per-CTA shares); 128-bit
+// ld.global.nc.L1::no_allocate loads, U in flight per thread, 4 CTAs per
+// SM.  Weight-0 ranges (TP duplicates) are never loaded.  Every square is
+// exact in fp64 and summed in fp64; CTA partials are combined by the last
+// CTA in a fixed order, so results are bit-reproducible run to run.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
