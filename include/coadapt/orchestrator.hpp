@@ -12,6 +12,7 @@
 #include <optional>
 #include <span>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -115,5 +116,30 @@ Command decide(std::span<const Candidate> candidates, std::optional<double> phi,
                const ConfigTuple& current, const ClockState& clock,
                const OrchestratorConfig& cfg,
                std::optional<double> current_throughput = std::nullopt);
+
+// ---- wire / disk formats ----
+
+// Profile CSV: header exactly
+//   d,t,p,global_batch,micro_batch,samples_per_sec,peak_mem_bytes,feasible
+// Numbers via format_double/parse_double, so save -> load is bit-exact.
+// ParseError names the line; ValidationError for invariant violations
+// (d*t*p differing between rows, B_g mod d*B_m != 0, duplicate keys).
+std::string profile_csv(const ThroughputProfile& profile);
+ThroughputProfile parse_profile_csv(std::string_view text,
+                                    const std::string& where);
+ThroughputProfile load_profile(const std::string& path);
+void save_profile(const std::string& path, const ThroughputProfile& profile);
+
+// Decision audit log: header
+//   step,time_s,phi,current_cfg,winner_cfg,current_score,winner_score,penalized,command
+struct DecisionRecord {
+  std::int64_t step = 0;
+  double time_s = 0.0;
+  std::optional<double> phi;  // written as nan when unavailable
+  Command command;
+  ConfigTuple current;
+};
+std::string decision_audit_csv(std::span<const DecisionRecord> rows);
+const char* command_name(CommandKind kind);
 
 }  // namespace coadapt

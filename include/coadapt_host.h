@@ -111,6 +111,40 @@ typedef struct coadapt_trace_row {
 } coadapt_trace_row;
 int coadapt_trace_csv(const coadapt_trace_row* rows, size_t n, char* buf,
                       size_t cap, size_t* needed);
+/* Profile CSV.  *count: in = capacity of out,
+ * out = number of entries.  Parse errors -> status 1 with the line number
+ * in coadapt_last_error(). */
+typedef struct coadapt_profile_entry {
+  int32_t d, t, p, reserved_;
+  int64_t global_batch;
+  int64_t micro_batch;
+  double samples_per_sec;
+  double peak_mem_bytes;
+  int32_t feasible;
+  int32_t reserved2_;
+} coadapt_profile_entry;
+int coadapt_profile_parse(const char* text, size_t len,
+                          coadapt_profile_entry* out, size_t* count,
+                          int* n_gpus);
+int coadapt_profile_format(const coadapt_profile_entry* entries, size_t n,
+                           char* buf, size_t cap, size_t* needed);
+int coadapt_profile_load(const char* path, coadapt_profile_entry* out,
+                         size_t* count, int* n_gpus);
+int coadapt_profile_save(const char* path, const coadapt_profile_entry* e,
+                         size_t n);
+
+/* Decision audit log, one row per decide() call */
+typedef struct coadapt_decision_row {
+  int64_t step;
+  double time_s;
+  double phi; /* NaN when unavailable */
+  coadapt_candidate current;
+  coadapt_candidate winner;
+  coadapt_command command;
+} coadapt_decision_row;
+int coadapt_decision_audit_csv(const coadapt_decision_row* rows, size_t n,
+                               char* buf, size_t cap, size_t* needed);
+
 /* format_double, io.hpp:13 */
 int coadapt_format_double(double v, char* buf, size_t cap);
 

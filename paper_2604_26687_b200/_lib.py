@@ -98,6 +98,18 @@ class CommandC(C.Structure):
                 ("current_score", C.c_double), ("penalized", C.c_int32), ("reserved_", C.c_int32)]
 
 
+class ProfileEntryC(C.Structure):
+    _fields_ = [("d", C.c_int32), ("t", C.c_int32), ("p", C.c_int32), ("reserved_", C.c_int32),
+                ("global_batch", C.c_int64), ("micro_batch", C.c_int64),
+                ("samples_per_sec", C.c_double), ("peak_mem_bytes", C.c_double),
+                ("feasible", C.c_int32), ("reserved2_", C.c_int32)]
+
+
+class DecisionRowC(C.Structure):
+    _fields_ = [("step", C.c_int64), ("time_s", C.c_double), ("phi", C.c_double),
+                ("current", CandidateC), ("winner", CandidateC), ("command", CommandC)]
+
+
 class TraceRowC(C.Structure):
     _fields_ = [("step", C.c_int64), ("tokens", C.c_int64), ("signal_raw", C.c_double),
                 ("noise_raw", C.c_double), ("ema_signal", C.c_double), ("ema_noise", C.c_double),
@@ -160,6 +172,11 @@ SIGNATURES = {
     "coadapt_decide": (I, [P, SZ, I, D, P, D, D, P, P]),
     "coadapt_trace_csv": (I, [P, SZ, P, SZ, P]),
     "coadapt_format_double": (I, [D, P, SZ]),
+    "coadapt_profile_parse": (I, [P, SZ, P, P, P]),
+    "coadapt_profile_format": (I, [P, SZ, P, SZ, P]),
+    "coadapt_profile_load": (I, [C.c_char_p, P, P, P]),
+    "coadapt_profile_save": (I, [C.c_char_p, P, SZ]),
+    "coadapt_decision_audit_csv": (I, [P, SZ, P, SZ, P]),
     "coadapt_simulate_micro_gradients": (I, [P, P, U64, I64, I, U64, P]),
 }
 

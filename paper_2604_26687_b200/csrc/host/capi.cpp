@@ -2,6 +2,7 @@
 // Exceptions are caught at the boundary and mapped to status codes
 // (errors.hpp:8-27 -> 1 / 1 / 2).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -288,6 +289,116 @@ int coadapt_trace_csv(const coadapt_trace_row* rows, size_t n, char* buf,
       std::memcpy(buf, s.data(), k);
       buf[k] = '\0';
     }
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+void profile_out(const coadapt::ThroughputProfile& prof,
+                 coadapt_profile_entry* out, size_t* count, int* n_gpus) {
+  const size_t cap = *count;
+  *count = prof.entries.size();
+  if (n_gpus) *n_gpus = prof.n_gpus;
+  if (!out) return;
+  size_t i = 0;
+  for (const auto& [c, e] : prof.entries) {
+    if (i >= cap) break;
+    std::memset(&out[i], 0, sizeof(out[i]));
+    out[i].d = c.strategy.d;
+    out[i].t = c.strategy.t;
+    out[i].p = c.strategy.p;
+    out[i].global_batch = c.global_batch;
+    out[i].micro_batch = c.micro_batch;
+    out[i].samples_per_sec = e.samples_per_second;
+    out[i].peak_mem_bytes = e.peak_memory;
+    out[i].feasible = e.feasible ? 1 : 0;
+    ++i;
+  }
+}
+
+coadapt::ThroughputProfile profile_in(const coadapt_profile_entry* e, size_t n) {
+  coadapt::ThroughputProfile prof;
+  for (size_t i = 0; i < n; ++i) {
+    const coadapt::ConfigTuple c{coadapt::ParallelStrategy{e[i].d, e[i].t, e[i].p},
+                                 e[i].global_batch, e[i].micro_batch};
+    if (prof.n_gpus == 0) prof.n_gpus = c.strategy.gpus();
+    coadapt::validate_config(c, prof.n_gpus);
+    if (!prof.entries
+             .emplace(c, coadapt::ThroughputEntry{e[i].samples_per_sec,
+                                                  e[i].peak_mem_bytes,
+                                                  e[i].feasible != 0})
+             .second)
+      throw coadapt::ValidationError("duplicate key " + c.label());
+  }
+  return prof;
+}
+
+void text_out(const std::string& s, char* buf, size_t cap, size_t* needed) {
+  if (needed) *needed = s.size();
+  if (buf && cap) {
+    const size_t k = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = '\0';
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int coadapt_profile_parse(const char* text, size_t len,
+                          coadapt_profile_entry* out, size_t* count,
+                          int* n_gpus) {
+  return guarded([&] {
+    if (!count || (len && !text)) throw coadapt::ValidationError("NULL argument");
+    profile_out(coadapt::parse_profile_csv(std::string_view(text, len), "profile.csv"),
+                out, count, n_gpus);
+  });
+}
+
+int coadapt_profile_format(const coadapt_profile_entry* e, size_t n, char* buf,
+                           size_t cap, size_t* needed) {
+  return guarded([&] {
+    if (n && !e) throw coadapt::ValidationError("NULL argument");
+    text_out(coadapt::profile_csv(profile_in(e, n)), buf, cap, needed);
+  });
+}
+
+int coadapt_profile_load(const char* path, coadapt_profile_entry* out,
+                         size_t* count, int* n_gpus) {
+  return guarded([&] {
+    if (!path || !count) throw coadapt::ValidationError("NULL argument");
+    profile_out(coadapt::load_profile(path), out, count, n_gpus);
+  });
+}
+
+int coadapt_profile_save(const char* path, const coadapt_profile_entry* e,
+                         size_t n) {
+  return guarded([&] {
+    if (!path || (n && !e)) throw coadapt::ValidationError("NULL argument");
+    coadapt::save_profile(path, profile_in(e, n));
+  });
+}
+
+int coadapt_decision_audit_csv(const coadapt_decision_row* rows, size_t n,
+                               char* buf, size_t cap, size_t* needed) {
+  return guarded([&] {
+    if (n && !rows) throw coadapt::ValidationError("NULL argument");
+    std::vector<coadapt::DecisionRecord> v(n);
+    for (size_t i = 0; i < n; ++i) {
+      v[i].step = rows[i].step;
+      v[i].time_s = rows[i].time_s;
+      if (!std::isnan(rows[i].phi)) v[i].phi = rows[i].phi;
+      v[i].current = cand(rows[i].current).config;
+      v[i].command.winner = cand(rows[i].winner).config;
+      v[i].command.kind = (coadapt::CommandKind)rows[i].command.kind;
+      v[i].command.current_score = rows[i].command.current_score;
+      v[i].command.winner_score = rows[i].command.winner_score;
+      v[i].command.penalized = rows[i].command.penalized != 0;
+    }
+    text_out(coadapt::decision_audit_csv(v), buf, cap, needed);
   });
 }
 

@@ -246,3 +246,80 @@ def decide(cands: Sequence[Candidate], phi: Optional[float], current: Candidate,
                                C.byref(_cfg(margin, max_growth, reconfig_cost, reference_batch)),
                                C.byref(out)))
     return Command(out.kind, out.winner_index, out.winner_score, out.current_score, bool(out.penalized))
+
+
+# ---------------------------------------------------------------- formats
+
+@dataclass(frozen=True)
+class ProfileEntry:
+    """One row of the throughput table."""
+    d: int
+    t: int
+    p: int
+    global_batch: int
+    micro_batch: int
+    samples_per_sec: float
+    peak_mem_bytes: float
+    feasible: bool
+
+    def _c(self) -> L.ProfileEntryC:
+        return L.ProfileEntryC(self.d, self.t, self.p, 0, self.global_batch, self.micro_batch,
+                               self.samples_per_sec, self.peak_mem_bytes, int(self.feasible), 0)
+
+
+def _entries_out(fn, *args):
+    n, g = C.c_size_t(0), C.c_int(0)
+    check(fn(*args, None, C.byref(n), C.byref(g)))
+    out = (L.ProfileEntryC * max(1, n.value))()
+    check(fn(*args, out, C.byref(n), C.byref(g)))
+    return [ProfileEntry(e.d, e.t, e.p, e.global_batch, e.micro_batch, e.samples_per_sec,
+                         e.peak_mem_bytes, bool(e.feasible)) for e in out[:n.value]], g.value
+
+
+def parse_profile_csv(text: str):
+    """-> (entries sorted by (S, B_g, B_m), n_gpus); ValidationError on bad rows."""
+    b = text.encode()
+    return _entries_out(lib().coadapt_profile_parse, b, len(b))
+
+
+def load_profile(path: str):
+    return _entries_out(lib().coadapt_profile_load, path.encode())
+
+
+def _text_out(fn, *args) -> str:
+    need = C.c_size_t()
+    check(fn(*args, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value + 1)
+    check(fn(*args, buf, need.value + 1, C.byref(need)))
+    return buf.value.decode()
+
+
+def profile_csv(entries: Sequence[ProfileEntry]) -> str:
+    arr = (L.ProfileEntryC * max(1, len(entries)))(*[e._c() for e in entries])
+    return _text_out(lib().coadapt_profile_format, arr, len(entries))
+
+
+def save_profile(path: str, entries: Sequence[ProfileEntry]) -> None:
+    arr = (L.ProfileEntryC * max(1, len(entries)))(*[e._c() for e in entries])
+    check(lib().coadapt_profile_save(path.encode(), arr, len(entries)))
+
+
+@dataclass
+class DecisionRow:
+    step: int
+    time_s: float
+    phi: Optional[float]
+    current: Candidate
+    winner: Candidate
+    command: Command
+
+
+def decision_audit_csv(rows: Sequence[DecisionRow]) -> str:
+    """SPEC.md:404-405 decision audit log."""
+    arr = (L.DecisionRowC * max(1, len(rows)))(*[
+        L.DecisionRowC(r.step, r.time_s, float("nan") if r.phi is None else r.phi, r.current._c(),
+                       r.winner._c(), L.CommandC(r.command.kind, r.command.winner_index,
+                                                 r.command.winner_score, r.command.current_score,
+                                                 int(r.command.penalized), 0))
+        for r in rows])
+    return _text_out(lib().coadapt_decision_audit_csv, arr, len(rows))
