@@ -503,19 +503,31 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
       : "memory");
 }
 
-template <int DT, int M>
+// Shape variants of the fused TMA kernel: (consumer warps, stage bytes).
+template <int V> struct TmaShape;
+template <> struct TmaShape<0> { static constexpr int NW = 12, kStageBytes = 49152; };
+template <> struct TmaShape<1> { static constexpr int NW = 16, kStageBytes = 49152; };
+template <> struct TmaShape<2> { static constexpr int NW = 8, kStageBytes = 32768; };
+template <> struct TmaShape<3> { static constexpr int NW = 8, kStageBytes = 49152; };
+template <> struct TmaShape<4> { static constexpr int NW = 16, kStageBytes = 57344; };
+
+template <int DT, int M, int V = 0>
 struct TmaCfg {
   static constexpr int ES = Elem<DT>::kSize;
   static constexpr int PV = Elem<DT>::kPerVec;
-  static constexpr int kStages = 3;
-  // ~64 KB per stage, tiles a multiple of 256 B (>= 4 KB for M <= 16)
-  static constexpr int kTile = (65536 / M) & ~255;
+  // 4 stages; chunk i -> stage i % 4 and consumer group i % 2, so every
+  // stage is always drained by the same group and each group observes every
+  // mbarrier phase of its stages (parity waits cannot alias).
+  static constexpr int kStages = 4;
+  // tiles a multiple of 256 B
+  static constexpr int kTile = (TmaShape<V>::kStageBytes / M) & ~255;
   static constexpr int P = kTile / ES;  // elements per chunk
   static constexpr int kStage = kTile * M;
   static constexpr int kSmem = kStages * kStage;
-  static constexpr int NW = 16;         // consumer warps
+  static constexpr int NW = TmaShape<V>::NW;  // consumer warps: 2 groups
   static constexpr int CT = NW * 32;
   static constexpr int NT = CT + 32;    // + 1 producer warp
+  static_assert(kStages % 2 == 0, "stages must split evenly between the groups");
 };
 
 struct ChunkMeta {
@@ -538,12 +550,12 @@ __device__ __forceinline__ float elem_at(const FusedArgs& args, int m,
 // and the M values of each element are summed in micro-batch order in fp32
 // (Megatron main_grad order), the sum squared in fp64.  The <16-byte edges
 // of a range come from global memory.
-template <int DT, int M, int GT, bool WEIGHTED>
+template <int DT, int M, int V, int GT, bool WEIGHTED>
 __device__ __forceinline__ void tma_consume_cols(const char* stage,
                                                  const FusedArgs& args,
                                                  const ChunkMeta& cm, int gt,
                                                  double* acc, double& gacc) {
-  using C = TmaCfg<DT, M>;
+  using C = TmaCfg<DT, M, V>;
   constexpr int VE = 16 / C::ES;
   constexpr int UP = DT;
   const uint64_t a = cm.a, b = cm.a + cm.n;
@@ -558,7 +570,12 @@ __device__ __forceinline__ void tma_consume_cols(const char* stage,
     for (int e = 0; e < C::PV; ++e) sum[e] = 0.0f;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const uint4 x = *reinterpret_cast<const uint4*>(stage + m * C::kTile + v * 16);
+      // volatile: keeps the M shared-memory loads in program order instead of
+      // hoisting all of them (register pressure, 12 warps hide the latency)
+      uint4 x;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                   : "r"(smem_u32(stage + m * C::kTile + v * 16)));
       float f[C::PV];
       unpack<UP>(x, f);
       if constexpr (WEIGHTED) {
@@ -594,15 +611,15 @@ __device__ __forceinline__ void tma_consume_cols(const char* stage,
   }
 }
 
-template <int DT, int M>
-__global__ void __launch_bounds__(TmaCfg<DT, M>::NT, 1)
+template <int DT, int M, int V>
+__global__ void __launch_bounds__(TmaCfg<DT, M, V>::NT, 1)
     fused_tma_kernel(const Range* __restrict__ R, int nr,
                      const uint64_t* __restrict__ prefix, uint64_t c_begin,
                      uint64_t c_end, const FusedArgs args, Sink sink) {
   // Two consumer groups of NW/2 warps take alternate chunks; every thread
   // owns whole positions of a chunk (tma_consume_cols), so per-thread state
   // is M fp64 accumulators and nothing is read twice from shared memory.
-  using C = TmaCfg<DT, M>;
+  using C = TmaCfg<DT, M, V>;
   constexpr int GW = C::NW / 2;  // warps per chunk
   extern __shared__ __align__(1024) char smem[];
   __shared__ uint64_t full[C::kStages], empty[C::kStages];
@@ -662,10 +679,10 @@ __global__ void __launch_bounds__(TmaCfg<DT, M>::NT, 1)
       mbar_wait(&full[st], (uint32_t)((i / C::kStages) & 1));
       const ChunkMeta cm = meta[st];
       if (cm.w == 1.0)
-        tma_consume_cols<DT, M, GW * 32, false>(smem + st * C::kStage, args, cm,
+        tma_consume_cols<DT, M, V, GW * 32, false>(smem + st * C::kStage, args, cm,
                                                 gt, acc, gtotal);
       else
-        tma_consume_cols<DT, M, GW * 32, true>(smem + st * C::kStage, args, cm,
+        tma_consume_cols<DT, M, V, GW * 32, true>(smem + st * C::kStage, args, cm,
                                                gt, acc, gtotal);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
@@ -1090,11 +1107,11 @@ struct TmaFn {
   int P = 0, smem = 0, nt = 0;
 };
 
-template <int DT, int M>
-TmaFn tma_fn() {
-  using C = TmaCfg<DT, M>;
+template <int DT, int M, int V>
+TmaFn tma_fn_v() {
+  using C = TmaCfg<DT, M, V>;
   TmaFn f;
-  f.fn = reinterpret_cast<void*>(&fused_tma_kernel<DT, M>);
+  f.fn = reinterpret_cast<void*>(&fused_tma_kernel<DT, M, V>);
   f.P = C::P;
   f.smem = C::kSmem;
   f.nt = C::NT;
@@ -1105,6 +1122,23 @@ TmaFn tma_fn() {
     attr = true;
   }
   return f;
+}
+
+// Best shape per M, measured on B200 (bf16, 8 GB, profiles/r01_tma_shapes.txt):
+// the chunk's vectors per tile vs the group's threads and the register cap
+// decide it (e.g. M=14: shape 4 7.06 TB/s vs shape 0 5.06).
+constexpr int kBestShape[17] = {4, 4, 4, 0, 4, 4, 0, 4, 0, 4, 0, 0, 0, 0, 4, 4, 4};
+
+template <int DT, int M>
+TmaFn tma_fn() {
+  static const char* e = getenv("COADAPT_TMA_SHAPE");  // development sweep
+  switch (e ? atoi(e) : kBestShape[M]) {
+    case 1: return tma_fn_v<DT, M, 1>();
+    case 2: return tma_fn_v<DT, M, 2>();
+    case 3: return tma_fn_v<DT, M, 3>();
+    case 4: return tma_fn_v<DT, M, 4>();
+    default: return tma_fn_v<DT, M, 0>();
+  }
 }
 
 template <int DT>
