@@ -204,6 +204,31 @@ int coadapt_gns_accumulate(coadapt_gns* g, const coadapt_plan* plan,
                            int dp_index, int micro, int flags,
                            double mean_scale_sq, void* stream);
 
+/* Fused DP gradient sync + gbar^2 over NVLink.
+ * replicas[q] (q < d <= 8) is DP replica q's gradient bucket mapped into this
+ * process (coadapt_ipc_open; the local one for q == dp_rank), all laid out
+ * as `plan` (a whole-bucket plan).  For this rank's slice [lo, hi) — the cut
+ * of coadapt_plan_create_slice(index = dp_rank, count = d) — writes
+ *   out_slice[i - lo] = RNE_dtype( scale * fp32(sum_q replicas[q][i]) )
+ * (replicas summed in index order) and adds sum w * out^2 (fp64) to gbar^2:
+ * the reduce-scatter of the Alg. 1 "standard gradient sync"
+ * and the norm of its result in one pass whose loads come
+ * from the peers' HBM over NVLink.  Bracket it with coadapt_gns_barrier so
+ * peers' buffers are complete before and untouched until every rank is done.
+ * Replaces: finalize_step(acc, span mean_gradient) gns.hpp:47-48 fed by a
+ * separate all-reduce. */
+/* handle (>= 64 B) of the allocation holding dev_ptr, and dev_ptr's offset
+ * in it (pass *offset to the peer; it adds it to the opened base) */
+int coadapt_ipc_handle(const void* dev_ptr, void* out, size_t len,
+                       uint64_t* offset);
+int coadapt_ipc_open(const void* handle, size_t len, int device, void** dev_ptr);
+int coadapt_ipc_close(void* dev_ptr);
+int coadapt_gns_barrier(coadapt_gns* g, void* stream);
+int coadapt_gns_reduce_scatter_sqnorm(coadapt_gns* g, const coadapt_plan* plan,
+                                      const void* const* replicas, int d,
+                                      int dp_rank, void* out_slice,
+                                      double scale, void* stream);
+
 /* NCCL over NVLink: sum the N+1 slots over all ranks (Alg. 1 AllReduce,
  * PAPER.md:443; the reference models it as summation). */
 int coadapt_nccl_unique_id(void* out, size_t len); /* len >= 128 */

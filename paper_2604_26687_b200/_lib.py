@@ -140,6 +140,11 @@ SIGNATURES = {
     "coadapt_gns_mean_sqnorm": (I, [P, P, P, P]),
     "coadapt_gns_fused_sqnorm_host": (I, [P, P, P, I, P]),
     "coadapt_gns_accumulate": (I, [P, P, P, P, I, I, I, D, P]),
+    "coadapt_ipc_handle": (I, [P, P, SZ, P]),
+    "coadapt_ipc_open": (I, [P, SZ, I, P]),
+    "coadapt_ipc_close": (I, [P]),
+    "coadapt_gns_barrier": (I, [P, P]),
+    "coadapt_gns_reduce_scatter_sqnorm": (I, [P, P, P, I, I, P, D, P]),
     "coadapt_nccl_unique_id": (I, [P, SZ]),
     "coadapt_gns_attach_nccl": (I, [P, I, I, P, SZ]),
     "coadapt_gns_allreduce": (I, [P, P]),

@@ -152,6 +152,7 @@ struct coadapt_gns {
   bool finalized = false;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  double* barrier_buf = nullptr;  // coadapt_gns_barrier scratch
   // host streaming (coadapt_gns_fused_sqnorm_host)
   void* staging = nullptr;  // kStages * 16 * kStageElems * es bytes
   size_t staging_bytes = 0;
@@ -543,6 +544,7 @@ int coadapt_gns_destroy(coadapt_gns* g) {
     DeviceGuard guard(g->device);
     cudaDeviceSynchronize();
     if (g->comm) ncclCommDestroy(g->comm);
+    if (g->barrier_buf) cudaFree(g->barrier_buf);
     if (g->slots) cudaFree(g->slots);
     if (g->partials) cudaFree(g->partials);
     if (g->ticket) cudaFree(g->ticket);
@@ -798,6 +800,117 @@ int coadapt_gns_accumulate(coadapt_gns* g, const coadapt_plan* p,
   CU(coadapt::dev::launch_accum(p->dtype, p->full, (int)p->full_host.size(),
                                 p->bucket_numel, a, sink, grid,
                                 static_cast<cudaStream_t>(stream)));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return COADAPT_OK;
+}
+
+int coadapt_ipc_handle(const void* dev_ptr, void* out, size_t len,
+                       uint64_t* offset) {
+  if (!dev_ptr || !out || len < sizeof(cudaIpcMemHandle_t))
+    return fail(COADAPT_E_VALIDATION, "ipc handle buffer must be >= 64 bytes");
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  std::memcpy(out, &h, sizeof(h));
+  if (offset) {
+    // the handle names the whole allocation (e.g. a caching-allocator
+    // block): report where dev_ptr sits in it (driver cuMemGetAddressRange)
+    using range_fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static range_fn fn = nullptr;
+    if (!fn) {
+      void* sym = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      CU(cudaGetDriverEntryPoint("cuMemGetAddressRange", &sym, cudaEnableDefault, &q));
+      if (!sym) return fail(COADAPT_E_CUDA, "cuMemGetAddressRange unavailable");
+      fn = reinterpret_cast<range_fn>(sym);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+      return fail(COADAPT_E_CUDA, "cuMemGetAddressRange failed");
+    *offset = reinterpret_cast<uint64_t>(dev_ptr) - base;
+  }
+  return COADAPT_OK;
+}
+
+int coadapt_ipc_open(const void* handle, size_t len, int device,
+                     void** dev_ptr) {
+  if (!handle || !dev_ptr || len < sizeof(cudaIpcMemHandle_t))
+    return fail(COADAPT_E_VALIDATION, "bad ipc handle");
+  GUARD(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  CU(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return COADAPT_OK;
+}
+
+int coadapt_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return COADAPT_OK;
+  CU(cudaIpcCloseMemHandle(dev_ptr));
+  return COADAPT_OK;
+}
+
+int coadapt_gns_barrier(coadapt_gns* g, void* stream) {
+  if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
+  if (!g->comm || g->nranks == 1) return COADAPT_OK;
+  GUARD(g->device);
+  // a one-element all-reduce on the stream orders every rank's prior work
+  // before everything enqueued after it (no host round trip)
+  if (!g->barrier_buf) CU(cudaMalloc(&g->barrier_buf, sizeof(double)));
+  NC(ncclAllReduce(g->barrier_buf, g->barrier_buf, 1, ncclFloat64, ncclSum,
+                   g->comm, static_cast<cudaStream_t>(stream)));
+  return COADAPT_OK;
+}
+
+int coadapt_gns_reduce_scatter_sqnorm(coadapt_gns* g, const coadapt_plan* p,
+                                      const void* const* replicas, int d,
+                                      int dp_rank, void* out_slice,
+                                      double scale, void* stream) {
+  if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
+  if (p->device != g->device)
+    return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
+  if (p->is_slice)
+    return fail(COADAPT_E_VALIDATION, "reduce-scatter needs a whole-bucket plan");
+  if (p->dtype == COADAPT_FP64)
+    return fail(COADAPT_E_VALIDATION, "fp64 buckets are not supported here");
+  if (d < 1 || d > coadapt::dev::kMaxReplicas || dp_rank < 0 || dp_rank >= d)
+    return fail(COADAPT_E_VALIDATION, "need 1 <= d <= 8 and 0 <= dp_rank < d");
+  if (!replicas || (p->bucket_numel && !out_slice))
+    return fail(COADAPT_E_VALIDATION, "replicas/out_slice is NULL");
+  if (!(scale == scale) || std::isinf(scale))
+    return fail(COADAPT_E_VALIDATION, "scale must be finite");
+  coadapt::dev::RSArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int q = 0; q < d; ++q) {
+    if (!replicas[q] && p->bucket_numel)
+      return fail(COADAPT_E_VALIDATION, "replica pointer is NULL");
+    if (reinterpret_cast<uintptr_t>(replicas[q]) & 15)
+      return fail(COADAPT_E_VALIDATION, "replica buffers must be 16-byte aligned");
+    a.rep[q] = replicas[q];
+  }
+  if (reinterpret_cast<uintptr_t>(out_slice) & 15)
+    return fail(COADAPT_E_VALIDATION, "out_slice must be 16-byte aligned");
+  // the same cut as coadapt_plan_create_slice
+  const uint64_t n = p->bucket_numel;
+  auto cut = [&](int i) -> uint64_t {
+    if (i >= d) return n;
+    return (uint64_t)((unsigned __int128)n * i / d) & ~uint64_t(63);
+  };
+  const uint64_t lo = cut(dp_rank), hi = cut(dp_rank + 1);
+  a.d = d;
+  a.scale = (float)scale;
+  a.out = out_slice;
+  a.gslot = g->N;
+  GUARD(g->device);
+  coadapt_plan* pm = const_cast<coadapt_plan*>(p);
+  if (int rc = plan_full(pm)) return rc;
+  if (hi <= lo) return COADAPT_OK;
+  const int grid =
+      grid_for(g->device, coadapt::dev::occupancy_rs(p->dtype), hi - lo);
+  if (int rc = ensure_partials(g, (size_t)grid)) return rc;
+  Sink sink{g->partials, g->ticket, g->slots};
+  CU(coadapt::dev::launch_rs(p->dtype, p->full, (int)p->full_host.size(), lo,
+                             hi, a, sink, grid,
+                             static_cast<cudaStream_t>(stream)));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return COADAPT_OK;
 }

@@ -83,6 +83,20 @@ int occupancy_accum(int dtype);
 cudaError_t launch_accum(int dtype, const Range* full, int nfull, uint64_t numel,
                          const AccumArgs& a, Sink sink, int grid, cudaStream_t s);
 
+// Fused DP reduce-scatter + gbar^2 over peer (NVLink) memory.
+constexpr int kMaxReplicas = 8;
+struct RSArgs {
+  const void* rep[kMaxReplicas];  // replica buckets (peer or local pointers)
+  int32_t d;
+  float scale;
+  void* out;                      // this rank's slice, element lo at out[0]
+  int32_t gslot;
+};
+int occupancy_rs(int dtype);
+cudaError_t launch_rs(int dtype, const Range* full, int nfull, uint64_t lo,
+                      uint64_t hi, const RSArgs& a, Sink sink, int grid,
+                      cudaStream_t s);
+
 struct FinalizeArgs {
   const double* slots;
   int32_t n;               // N; slots[N] = gbar^2

@@ -841,6 +841,156 @@ __global__ void __launch_bounds__(NT, 3)
   last_cta_combine<NT>(sink, mean ? 2 : 1, out_slot, out_scale, red);
 }
 
+// ---------------------------------------------------------------- KR
+//
+// Fused DP reduce-scatter + mean-gradient norm over NVLink (SURVEY §8f row
+// f2).  DP replica q's accumulated gradient bucket is mapped into this
+// process (CUDA IPC peer pointer, or local for q == this rank); for every
+// element of this rank's slice [lo, hi):
+//   out[i - lo] = RNE_dtype( scale * fp32( sum_{q = 0..d-1} rep_q[i] ) )
+// (replicas summed in fixed order) and gbar^2 += w * out^2 in fp64 — the
+// synchronised mean gradient is produced and its norm taken in ONE pass, the
+// loads coming straight from the peers' HBM over NVLink.
+
+__device__ __forceinline__ uint4 ld_peer(const uint4* p) {  // no .nc on peer memory
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+template <int DT>
+__device__ __forceinline__ void pack(const float* f, uint4& v);
+template <>
+__device__ __forceinline__ void pack<COADAPT_BF16>(const float* f, uint4& v) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    w[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  v = make_uint4(w[0], w[1], w[2], w[3]);
+}
+template <>
+__device__ __forceinline__ void pack<COADAPT_FP16>(const float* f, uint4& v) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __half2 h = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
+    w[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  v = make_uint4(w[0], w[1], w[2], w[3]);
+}
+template <>
+__device__ __forceinline__ void pack<COADAPT_FP32>(const float* f, uint4& v) {
+  v = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]),
+                 __float_as_uint(f[2]), __float_as_uint(f[3]));
+}
+
+template <int DT>
+__device__ __forceinline__ float round_dt(float x) {
+  if constexpr (DT == COADAPT_BF16) return __bfloat162float(__float2bfloat16_rn(x));
+  else if constexpr (DT == COADAPT_FP16) return __half2float(__float2half_rn(x));
+  else return x;
+}
+
+template <int DT>
+__device__ __forceinline__ void store_dt(char* base, uint64_t i, float x) {
+  if constexpr (DT == COADAPT_BF16)
+    reinterpret_cast<__nv_bfloat16*>(base)[i] = __float2bfloat16_rn(x);
+  else if constexpr (DT == COADAPT_FP16)
+    reinterpret_cast<__half*>(base)[i] = __float2half_rn(x);
+  else
+    reinterpret_cast<float*>(base)[i] = x;
+}
+
+template <int DT, int NT, int U>
+__global__ void __launch_bounds__(NT, 2)
+    rs_kernel(const Range* __restrict__ R, int nr, uint64_t lo, uint64_t hi,
+              const __grid_constant__ RSArgs a, Sink sink) {
+  constexpr int ES = Elem<DT>::kSize, PV = Elem<DT>::kPerVec;
+  constexpr uint64_t CE = (uint64_t)U * NT * PV;
+  __shared__ double red[32];
+  const uint64_t n = hi - lo, nchunks = (n + CE - 1) / CE;
+  char* out = static_cast<char*>(a.out);
+  double g = 0.0;
+  int k = 0;
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint64_t e0 = lo + c * CE, e1 = min(e0 + CE, hi);
+    while (k + 1 < nr && R[k + 1].abs_begin <= e0) ++k;
+    for (int kk = k; kk < nr && R[kk].abs_begin < e1; ++kk) {
+      const uint64_t pa = max(R[kk].abs_begin, e0);
+      const uint64_t pb = min(R[kk].abs_begin + R[kk].len, e1);
+      if (pa >= pb) continue;
+      const double w = R[kk].weight;
+      const uint64_t A0 = (pa + PV - 1) / PV * PV, A1 = pb / PV * PV;
+      auto scalar = [&](uint64_t i) {
+        float s = 0.0f;
+        for (int q = 0; q < a.d; ++q)
+          s = __fadd_rn(s, elem_f32<DT>(reinterpret_cast<uintptr_t>(a.rep[q]) + i * ES));
+        const float o = round_dt<DT>(__fmul_rn(s, a.scale));
+        store_dt<DT>(out, i - lo, o);
+        const double od = o;
+        g = fma(w * od, od, g);
+      };
+      if (A1 <= A0) {
+        for (uint64_t i = pa + threadIdx.x; i < pb; i += NT) scalar(i);
+        continue;
+      }
+      if (pa + threadIdx.x < A0) scalar(pa + threadIdx.x);
+      if (A1 + threadIdx.x < pb) scalar(A1 + threadIdx.x);
+      const uint64_t nv = (A1 - A0) / PV;
+      for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)U * NT) {
+        float sum[U][PV];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+#pragma unroll
+          for (int e = 0; e < PV; ++e) sum[j][e] = 0.0f;
+        for (int q = 0; q < a.d; ++q) {
+          const uint4* src = reinterpret_cast<const uint4*>(
+              static_cast<const char*>(a.rep[q]) + A0 * ES);
+          uint4 r[U];
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            const uint64_t v = v0 + (uint64_t)j * NT;
+            r[j] = v < nv ? ld_peer(src + v) : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            float f[PV];
+            unpack<DT>(r[j], f);
+#pragma unroll
+            for (int e = 0; e < PV; ++e) sum[j][e] = __fadd_rn(sum[j][e], f[e]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const uint64_t v = v0 + (uint64_t)j * NT;
+          if (v >= nv) continue;
+          float o[PV];
+          double gl = 0.0;
+#pragma unroll
+          for (int e = 0; e < PV; ++e) {
+            o[e] = round_dt<DT>(__fmul_rn(sum[j][e], a.scale));
+            const double od = o[e];
+            gl = fma(od, od, gl);
+          }
+          uint4 ov;
+          pack<DT>(o, ov);
+          st_stream(reinterpret_cast<uint4*>(out + (A0 - lo) * ES) + v, ov);
+          g = fma(w, gl, g);
+        }
+      }
+    }
+  }
+  const double vg = block_sum<NT>(g, red);
+  if (threadIdx.x == 0) sink.partials[blockIdx.x] = vg;
+  __shared__ int32_t out_slot[1];
+  if (threadIdx.x == 0) out_slot[0] = a.gslot;
+  last_cta_combine<NT>(sink, 1, out_slot, nullptr, red);
+}
+
 // ---------------------------------------------------------------- K3
 
 struct DevState {  // == coadapt_gns_state
@@ -1221,6 +1371,30 @@ void* accum_fn(int dtype) {
 }  // namespace
 
 int occupancy_accum(int dtype) { return occupancy_of(accum_fn(dtype), kNTA); }
+
+namespace {
+constexpr int kNTR = 256, kUR = 2;
+void* rs_fn(int dtype) {
+  switch (dtype) {
+    case COADAPT_BF16: return reinterpret_cast<void*>(&rs_kernel<COADAPT_BF16, kNTR, kUR>);
+    case COADAPT_FP16: return reinterpret_cast<void*>(&rs_kernel<COADAPT_FP16, kNTR, kUR>);
+    case COADAPT_FP32: return reinterpret_cast<void*>(&rs_kernel<COADAPT_FP32, kNTR, kUR>);
+  }
+  return nullptr;
+}
+}  // namespace
+
+int occupancy_rs(int dtype) { return occupancy_of(rs_fn(dtype), kNTR); }
+
+cudaError_t launch_rs(int dtype, const Range* full, int nfull, uint64_t lo,
+                      uint64_t hi, const RSArgs& a, Sink sink, int grid,
+                      cudaStream_t s) {
+  void* fn = rs_fn(dtype);
+  if (!fn) return cudaErrorInvalidValue;
+  void* args[] = {(void*)&full, (void*)&nfull, (void*)&lo, (void*)&hi,
+                  (void*)&a, (void*)&sink};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(kNTR), args, 0, s);
+}
 
 cudaError_t launch_accum(int dtype, const Range* full, int nfull, uint64_t numel,
                          const AccumArgs& a, Sink sink, int grid,

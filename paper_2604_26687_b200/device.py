@@ -157,6 +157,19 @@ class GnsDevice:
                                            _ptr(micro_grad), int(dp_index), int(micro), flags,
                                            float(mean_scale_sq), _stream(stream)))
 
+    def barrier(self, stream=None) -> None:
+        """Stream-ordered cross-rank barrier (1-element NCCL all-reduce)."""
+        check(lib().coadapt_gns_barrier(self.handle, _stream(stream)))
+
+    def reduce_scatter_sqnorm(self, plan: BucketPlan, replicas: Sequence, dp_rank: int, out_slice,
+                              scale: float, stream=None) -> None:
+        """Fused DP reduce-scatter + gbar^2 over NVLink (peer pointers from
+        ipc_open; the local replica by pointer)."""
+        k = len(replicas)
+        ptrs = (C.c_void_p * max(1, k))(*[_ptr(r) for r in replicas])
+        check(lib().coadapt_gns_reduce_scatter_sqnorm(self.handle, plan.handle, ptrs, k, int(dp_rank),
+                                                      _ptr(out_slice), float(scale), _stream(stream)))
+
     def mean_sqnorm(self, plan: BucketPlan, mean_grad, stream=None) -> None:
         check(lib().coadapt_gns_mean_sqnorm(self.handle, plan.handle, _ptr(mean_grad), _stream(stream)))
 
@@ -198,6 +211,34 @@ class GnsDevice:
             self.close()
         except Exception:
             pass
+
+
+def ipc_handle(t: torch.Tensor) -> tuple:
+    """(64-byte CUDA IPC handle of the allocation holding `t`, offset of
+    t.data_ptr() inside it) — send both to the peer (ipc_open)."""
+    buf = C.create_string_buffer(64)
+    off = C.c_uint64()
+    check(lib().coadapt_ipc_handle(t.data_ptr(), buf, 64, C.byref(off)))
+    return buf.raw, off.value
+
+
+def ipc_open(handle, device: int) -> tuple:
+    """-> (device pointer to the peer tensor, base pointer to ipc_close)"""
+    raw, off = handle
+    ptr = C.c_void_p()
+    hb = C.create_string_buffer(bytes(raw), len(raw))
+    check(lib().coadapt_ipc_open(hb, len(raw), int(device), C.byref(ptr)))
+    return int(ptr.value) + int(off), int(ptr.value)
+
+
+def ipc_close(ptr: int) -> None:
+    check(lib().coadapt_ipc_close(C.c_void_p(ptr)))
+
+
+def dp_slice(numel: int, d: int, r: int) -> tuple:
+    """[lo, hi) of DP slice r of d (the cut of coadapt_plan_create_slice)."""
+    cut = lambda i: numel if i >= d else (numel * i // d) & ~63
+    return cut(r), cut(r + 1)
 
 
 def nccl_unique_id() -> bytes:

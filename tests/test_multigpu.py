@@ -112,3 +112,20 @@ def test_nccl_two_gpus_matches_one_gpu():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     rep = json.loads(lines[-1])
     assert rep["ok"], rep
+
+
+@pytest.mark.gpu
+def test_fused_reduce_scatter_norm_over_nvlink():
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs (gpurun --gpus 2)")
+    world = 4 if n >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29900 + os.getpid() % 90),
+           os.path.join(HERE, "mp_rs_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    rep = json.loads(lines[-1])
+    assert rep["ok"], rep
