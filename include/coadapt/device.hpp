@@ -71,6 +71,17 @@ class GnsDevicePlan {
                     std::span<const void* const> buckets, void* stream);
   void record_mean_gradient(const BucketLayout& layout, const void* mean,
                             void* stream);
+  // Trainer form (§8 f1): main_grad (+)= grad (fp32) with s_m fused in; on
+  // the last micro-batch of a d == 1 step also gbar^2 (mean_scale_sq * |main|^2).
+  void accumulate(const BucketLayout& layout, float* main_grad,
+                  const void* micro_grad, int dp_index, int micro, bool first,
+                  bool last_mean, double mean_scale_sq, void* stream);
+  // Fused DP reduce-scatter + gbar^2 over NVLink (§8 f2); replicas are the
+  // DP replicas' buckets mapped into this process (CUDA IPC).
+  void reduce_scatter_mean(const BucketLayout& layout,
+                           std::span<const void* const> replicas, int dp_rank,
+                           void* out_slice, double scale, void* stream);
+  void barrier(void* stream);
   void attach_nccl(int nranks, int rank, std::span<const unsigned char> id);
   void allreduce(void* stream);
   void finalize(std::int64_t tokens_this_step, void* stream);

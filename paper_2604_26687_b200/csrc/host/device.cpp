@@ -128,6 +128,29 @@ void GnsDevicePlan::record_mean_gradient(const BucketLayout& layout,
   check(coadapt_gns_mean_sqnorm(g_, layout.handle(), mean, stream));
 }
 
+void GnsDevicePlan::accumulate(const BucketLayout& layout, float* main_grad,
+                               const void* micro_grad, int dp_index, int micro,
+                               bool first, bool last_mean, double mean_scale_sq,
+                               void* stream) {
+  const int flags = (first ? COADAPT_ACC_FIRST : 0) |
+                    (last_mean ? COADAPT_ACC_LAST_MEAN : 0);
+  check(coadapt_gns_accumulate(g_, layout.handle(), main_grad, micro_grad,
+                               dp_index, micro, flags, mean_scale_sq, stream));
+}
+
+void GnsDevicePlan::reduce_scatter_mean(const BucketLayout& layout,
+                                        std::span<const void* const> replicas,
+                                        int dp_rank, void* out_slice,
+                                        double scale, void* stream) {
+  check(coadapt_gns_reduce_scatter_sqnorm(g_, layout.handle(), replicas.data(),
+                                          (int)replicas.size(), dp_rank,
+                                          out_slice, scale, stream));
+}
+
+void GnsDevicePlan::barrier(void* stream) {
+  check(coadapt_gns_barrier(g_, stream));
+}
+
 void GnsDevicePlan::attach_nccl(int nranks, int rank,
                                 std::span<const unsigned char> id) {
   check(coadapt_gns_attach_nccl(g_, nranks, rank, id.data(), id.size()));
