@@ -964,7 +964,15 @@ int coadapt_gns_finalize(coadapt_gns* g, int64_t tokens, void* stream) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   CU(cudaMemcpyAsync(g->result_host, g->result, sizeof(coadapt_gns_result),
                      cudaMemcpyDeviceToHost, s));
-  CU(cudaEventRecord(g->result_ready, s));
+  // Under stream capture a plain record only orders nodes inside the graph;
+  // an external record node makes every replay signal result_ready, so
+  // read_result() after graph.replay() waits for that replay's D2H.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(s, &cap));
+  if (cap == cudaStreamCaptureStatusActive)
+    CU(cudaEventRecordWithFlags(g->result_ready, s, cudaEventRecordExternal));
+  else
+    CU(cudaEventRecord(g->result_ready, s));
   g->finalized = true;
   return COADAPT_OK;
 }
