@@ -110,6 +110,40 @@ class DecisionRowC(C.Structure):
                 ("current", CandidateC), ("winner", CandidateC), ("command", CommandC)]
 
 
+MAXD = 4  # COADAPT_RESHARD_MAX_DIMS
+
+
+class TensorDeclC(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("ndim", C.c_int32), ("tp_axis", C.c_int32),
+                ("shape", C.c_int64 * MAXD)]
+
+
+class ReshardModelC(C.Structure):
+    _fields_ = [("layers", C.c_int32), ("n_tensors", C.c_int32), ("tensors", C.POINTER(TensorDeclC)),
+                ("optimizer_state_multiplier", C.c_int32), ("param_bytes", C.c_int32),
+                ("state_bytes", C.c_int32), ("reserved_", C.c_int32)]
+
+
+class ShardC(C.Structure):
+    _fields_ = [("layer", C.c_int32), ("tensor", C.c_int32), ("owner", C.c_int32),
+                ("canonical", C.c_int32), ("global_shape", C.c_int64 * MAXD),
+                ("global_offset", C.c_int64 * MAXD), ("local_shape", C.c_int64 * MAXD),
+                ("pack_offset", C.c_uint64), ("ndim", C.c_int32), ("reserved_", C.c_int32)]
+
+
+class MoveC(C.Structure):
+    _fields_ = [("src_rank", C.c_int32), ("dst_rank", C.c_int32), ("layer", C.c_int32),
+                ("tensor", C.c_int32), ("offset", C.c_int64 * MAXD), ("extent", C.c_int64 * MAXD),
+                ("bytes", C.c_uint64), ("local", C.c_int32), ("ndim", C.c_int32)]
+
+
+class ReshardInfoC(C.Structure):
+    _fields_ = [("n_moves", C.c_uint64), ("total_bytes", C.c_uint64),
+                ("max_bytes_per_rank", C.c_uint64), ("local_bytes", C.c_uint64),
+                ("src_ranks", C.c_int32), ("dst_ranks", C.c_int32),
+                ("src_max_pack_numel", C.c_uint64), ("dst_max_pack_numel", C.c_uint64)]
+
+
 class TraceRowC(C.Structure):
     _fields_ = [("step", C.c_int64), ("tokens", C.c_int64), ("signal_raw", C.c_double),
                 ("noise_raw", C.c_double), ("ema_signal", C.c_double), ("ema_noise", C.c_double),
@@ -183,6 +217,16 @@ SIGNATURES = {
     "coadapt_profile_save": (I, [C.c_char_p, P, SZ]),
     "coadapt_decision_audit_csv": (I, [P, SZ, P, SZ, P]),
     "coadapt_simulate_micro_gradients": (I, [P, P, U64, I64, I, U64, P]),
+    # coadapt_reshard.h
+    "coadapt_reshard_plan_create": (I, [P, P, P, I, P]),
+    "coadapt_reshard_plan_destroy": (I, [P]),
+    "coadapt_reshard_plan_info": (I, [P, P]),
+    "coadapt_reshard_moves": (I, [P, P, P]),
+    "coadapt_reshard_shards": (I, [P, I, P, P]),
+    "coadapt_reshard_pack_numel": (I, [P, I, I, P]),
+    "coadapt_reshard_plan_csv": (I, [P, P, SZ, P]),
+    "coadapt_reshard_latency": (I, [P, D, D, P]),
+    "coadapt_reshard_execute": (I, [P, I, P, SZ, P, SZ, I, I, P]),
 }
 
 _lib = None
@@ -213,9 +257,9 @@ def check(rc: int) -> None:
 
 
 def header_symbols() -> list[str]:
-    """Every function declared in include/coadapt_cuda.h and coadapt_host.h."""
+    """Every function declared in the C-ABI headers under include/."""
     names = []
-    for h in ("coadapt_cuda.h", "coadapt_host.h"):
+    for h in ("coadapt_cuda.h", "coadapt_host.h", "coadapt_reshard.h"):
         text = open(os.path.join(INCLUDE_DIR, h)).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         names += re.findall(r"\b(coadapt_[a-z0-9_]+)\s*\(", text)

@@ -39,6 +39,8 @@ int fail(int code, const std::string& msg) {
 namespace coadapt_capi {
 // used by the C++-API bindings (host/capi.cpp) to share the message slot
 void set_error(const char* msg) { g_err = msg ? msg : ""; }
+// kernels launched from the other translation units (reshard.cu)
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace coadapt_capi
 
 namespace {

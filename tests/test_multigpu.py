@@ -129,3 +129,24 @@ def test_fused_reduce_scatter_norm_over_nvlink():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     rep = json.loads(lines[-1])
     assert rep["ok"], rep
+
+
+@pytest.mark.gpu
+def test_reshard_pull_over_nvlink():
+    """§8 f4: every rank pulls its new shards from the peers' packs (CUDA
+    IPC) — all strategy pairs of the world size, bit-exact vs the oracle,
+    plus a TP -> PP round trip at 0.5 GB per rank with the pull bandwidth."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs (gpurun --gpus 2)")
+    world = 4 if n >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29400 + os.getpid() % 90),
+           os.path.join(HERE, "mp_reshard_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    rep = json.loads(lines[-1])
+    print(json.dumps(rep))
+    assert rep["ok"], rep
