@@ -53,3 +53,105 @@ def test_c1_125m_fp32_d2_full_step():
     assert abs(parts[-1] - g2_ref) <= 1e-12 * g2_ref
     st = O.finalize_step(s_ref, g2_ref, d * M * 2)
     assert abs(r.b_simple - st.noise / st.signal) <= 1e-9 * abs(st.noise / st.signal)
+
+
+def _torch_sqnorm(b, segments, chunk=1 << 28):
+    """independent fp64 reference: torch, chunked, weights applied"""
+    tot = 0.0
+    for o, k, w in segments:
+        if w == 0.0:
+            continue
+        acc = torch.zeros((), dtype=torch.float64, device=b.device)
+        for c in range(o, o + k, chunk):
+            x = b[c:min(c + chunk, o + k)].to(torch.float64)
+            acc += torch.dot(x, x)
+        tot += w * acc.item()
+    return tot
+
+
+def test_c2_3b_bf16_d8_full_step():
+    """C2: Llama-3.2-3B bf16, (d,t,p) = (8,1,1), M = 8 — all 64 micro-buckets
+    (3.21 G elements each) through the batched K1 and all 8 mean slices
+    through K2, against an independent chunked torch fp64 reduction."""
+    from paper_2604_26687_b200 import _lib as L
+    from paper_2604_26687_b200 import device as D
+    from paper_2604_26687_b200 import layout as Lay
+    torch.cuda.set_device(0)
+    spec = Lay.llama32_3b()
+    d, M, seed = 8, 8, 0xC2
+    lays = Lay.world_layouts(spec, d, 1, 1)
+    unit = Lay.noise_unit_for(512.0, 2)
+    g = D.GnsDevice(d, M, d * M * 2, 0)
+    g.begin_step()
+    lay = lays[0]  # t = p = 1: every rank holds the whole model
+    plan = D.BucketPlan(lay.segments, lay.numel, L.BF16, 0)
+    bufs = [torch.empty(lay.numel, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    s_ref = np.zeros(d * M)
+    for i_d in range(d):
+        for m0 in range(0, M, 2):
+            for j in range(2):
+                D.synth_fill(bufs[j], lay.gen, seed, i_d * M + m0 + j, Lay.G0, unit)
+            g.micro_sqnorm_batched(plan, bufs, [i_d, i_d], [m0, m0 + 1])
+            for j in range(2):
+                s_ref[i_d * M + m0 + j] = _torch_sqnorm(bufs[j], lay.segments)
+    mean = bufs[0]
+    D.synth_mean_fill(mean, lay.gen, seed, 0, d * M, Lay.G0, unit)
+    for i_d in range(d):
+        sl = D.BucketPlan(lay.segments, lay.numel, L.BF16, 0, slice_index=i_d, slice_count=d)
+        g.mean_sqnorm(sl, mean)
+    g2_ref = _torch_sqnorm(mean, lay.segments)
+    g.finalize(d * M * 2 * 4096)
+    r = g.result()
+    parts = g.partials()
+    assert np.allclose(parts[:-1], s_ref, rtol=1e-12, atol=0)
+    assert abs(parts[-1] - g2_ref) <= 1e-12 * g2_ref
+    st = O.finalize_step(parts[:-1], parts[-1], d * M * 2)
+    assert r.b_simple == st.noise / st.signal or abs(r.b_simple - st.noise / st.signal) <= 1e-12 * abs(
+        st.noise / st.signal)
+
+
+def test_c3_7b_bf16_d2t2p2_layout_invariance_full_size():
+    """C3: Llama-2-7B bf16, (d,t,p) = (2,2,2) with TP-replicated norm dedup.
+    Size-independent property at full size: the 8 ranks' shard norms
+    (weight-0 duplicates skipped) sum to the norm of the unsharded 6.74 G
+    element gradient, for every micro-batch and for the synchronised mean
+    (DP slices) — i.e. the dedup weights and the (d,t,p) partition are
+    exact."""
+    from paper_2604_26687_b200 import _lib as L
+    from paper_2604_26687_b200 import device as D
+    from paper_2604_26687_b200 import layout as Lay
+    torch.cuda.set_device(0)
+    spec = Lay.llama2_7b()
+    d, t, p, M, seed = 2, 2, 2, 2, 0xC3
+    unit = Lay.noise_unit_for(256.0, 2)
+    world = Lay.world_layouts(spec, d, t, p)
+    whole = Lay.world_layouts(spec, 1, 1, 1)[0]
+    gw = D.GnsDevice(d, M, d * M * 2, 0)
+    gu = D.GnsDevice(d, M, d * M * 2, 0)
+    gw.begin_step()
+    gu.begin_step()
+    plan_u = D.BucketPlan(whole.segments, whole.numel, L.BF16, 0)
+    big = torch.empty(whole.numel, dtype=torch.bfloat16, device="cuda")
+    shard = torch.empty(max(l.numel for l in world), dtype=torch.bfloat16, device="cuda")
+    for i_d in range(d):
+        for m in range(M):
+            D.synth_fill(big, whole.gen, seed, i_d * M + m, Lay.G0, unit)
+            gu.micro_sqnorm(plan_u, big, i_d, m)
+    for lay in world:
+        i_d = lay.coords[0]
+        plan = D.BucketPlan(lay.segments, lay.numel, L.BF16, 0)
+        view = shard[:lay.numel]
+        for m in range(M):
+            D.synth_fill(view, lay.gen, seed, i_d * M + m, Lay.G0, unit)
+            gw.micro_sqnorm(plan, view, i_d, m)
+        D.synth_mean_fill(view, lay.gen, seed, 0, d * M, Lay.G0, unit)
+        sl = D.BucketPlan(lay.segments, lay.numel, L.BF16, 0, slice_index=i_d, slice_count=d)
+        gw.mean_sqnorm(sl, view)
+    D.synth_mean_fill(big, whole.gen, seed, 0, d * M, Lay.G0, unit)
+    gu.mean_sqnorm(plan_u, big)
+    a, b = gw.partials(), gu.partials()
+    assert np.allclose(a, b, rtol=1e-12, atol=0), (a, b)
+    # the replicated norms really were deduplicated: counting them on every
+    # TP rank would change s by their (nonzero) contribution
+    dup = sum(k for l in world for o, k, w in l.segments if w == 0.0)
+    assert dup > 0
