@@ -8,9 +8,10 @@
  *
  * Execution is device-side: every rank's training state is one "pack" per
  * state plane (coadapt/reshard.hpp describes the pack order);
- * coadapt_reshard_execute pulls each destination rank's regions from the
- * source packs — local pointers or NVLink peers mapped with
- * coadapt_ipc_open — in one kernel launch per plane.  Status codes and
+ * coadapt_reshard_execute copies the regions between packs — local
+ * pointers or NVLink peers mapped with coadapt_ipc_open — in one kernel
+ * launch per plane, each GPU either pulling its destination regions or
+ * pushing its source regions.  Status codes and
  * coadapt_last_error() as in coadapt_cuda.h.
  */
 #ifndef COADAPT_RESHARD_H_
@@ -104,13 +105,22 @@ int coadapt_reshard_latency(const coadapt_reshard_plan* plan,
                             double fixed_overhead_s, double* seconds);
 
 /* Execute the plan for one state plane of elem_bytes (1, 2, 4 or 8) bytes
- * per element.  src_packs[r] is source rank r's pack (NULL if this call
- * reads nothing from r), dst_packs[r] destination rank r's pack.
- * dst_rank >= 0 runs only the moves into that rank (one process per GPU);
- * dst_rank == -1 runs every move (all ranks' packs visible to this process,
- * e.g. virtual ranks on one GPU).  Source and destination packs must not
- * overlap.  Stream-ordered; one kernel launch (none if nothing to copy). */
-int coadapt_reshard_execute(coadapt_reshard_plan* plan, int dst_rank,
+ * per element.  src_packs[r] is source rank r's pack, dst_packs[r]
+ * destination rank r's pack (NULL where this call touches nothing).
+ *   role COADAPT_RESHARD_ALL:  every move (all packs visible to this
+ *                              process, e.g. virtual ranks on one GPU);
+ *   role COADAPT_RESHARD_PULL: the moves INTO `rank` — this GPU reads the
+ *                              sources (its own and NVLink peers);
+ *   role COADAPT_RESHARD_PUSH: the moves OUT OF `rank` — this GPU writes
+ *                              the destinations (its own and NVLink peers).
+ * Every rank running PULL (or every rank running PUSH) executes the plan
+ * exactly once.  Source and destination packs must not overlap; the caller
+ * orders the call after the sources are final and before they are freed
+ * (barriers).  Stream-ordered; one kernel launch (none if nothing to copy). */
+#define COADAPT_RESHARD_ALL 0
+#define COADAPT_RESHARD_PULL 1
+#define COADAPT_RESHARD_PUSH 2
+int coadapt_reshard_execute(coadapt_reshard_plan* plan, int role, int rank,
                             const void* const* src_packs, size_t n_src,
                             void* const* dst_packs, size_t n_dst,
                             int elem_bytes, int device, void* stream);

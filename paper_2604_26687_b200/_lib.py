@@ -226,7 +226,7 @@ SIGNATURES = {
     "coadapt_reshard_pack_numel": (I, [P, I, I, P]),
     "coadapt_reshard_plan_csv": (I, [P, P, SZ, P]),
     "coadapt_reshard_latency": (I, [P, D, D, P]),
-    "coadapt_reshard_execute": (I, [P, I, P, SZ, P, SZ, I, I, P]),
+    "coadapt_reshard_execute": (I, [P, I, I, P, SZ, P, SZ, I, I, P]),
 }
 
 _lib = None

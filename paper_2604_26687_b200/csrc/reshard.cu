@@ -217,7 +217,7 @@ struct coadapt_reshard_plan {
     CopyTask* dev = nullptr;
     uint32_t n = 0;
   };
-  std::map<std::pair<int, int>, Tasks> cache;  // (dst_rank or -1, elem_bytes)
+  std::map<std::tuple<int, int, int>, Tasks> cache;  // (role, rank, elem_bytes)
 };
 
 extern "C" {
@@ -371,7 +371,7 @@ int coadapt_reshard_latency(const coadapt_reshard_plan* p, double bw,
   });
 }
 
-int coadapt_reshard_execute(coadapt_reshard_plan* p, int dst_rank,
+int coadapt_reshard_execute(coadapt_reshard_plan* p, int role, int rank,
                             const void* const* src_packs, size_t n_src,
                             void* const* dst_packs, size_t n_dst,
                             int elem_bytes, int device, void* stream) {
@@ -384,13 +384,23 @@ int coadapt_reshard_execute(coadapt_reshard_plan* p, int dst_rank,
     return fail(COADAPT_E_VALIDATION,
                 "reshard: need " + std::to_string(S) + " source and " +
                     std::to_string(D) + " destination pack slots");
-  if (dst_rank < -1 || dst_rank >= D)
-    return fail(COADAPT_E_VALIDATION, "reshard: dst_rank out of range");
+  if (role != COADAPT_RESHARD_ALL && role != COADAPT_RESHARD_PULL &&
+      role != COADAPT_RESHARD_PUSH)
+    return fail(COADAPT_E_VALIDATION, "reshard: unknown role");
+  if (role == COADAPT_RESHARD_ALL) rank = -1;
+  if (role == COADAPT_RESHARD_PULL && (rank < 0 || rank >= D))
+    return fail(COADAPT_E_VALIDATION, "reshard: destination rank out of range");
+  if (role == COADAPT_RESHARD_PUSH && (rank < 0 || rank >= S))
+    return fail(COADAPT_E_VALIDATION, "reshard: source rank out of range");
+  auto mine = [&](const R::Move& m) {
+    return role == COADAPT_RESHARD_ALL ||
+           (role == COADAPT_RESHARD_PULL ? m.dst_rank : m.src_rank) == rank;
+  };
   // every pack this call touches must be present, and no source pack may
   // overlap a destination pack (the pull reads sources while writing)
   std::vector<char> need_src(S, 0), need_dst(D, 0);
   for (const auto& m : p->plan.moves)
-    if (dst_rank < 0 || m.dst_rank == dst_rank) {
+    if (mine(m)) {
       need_src[m.src_rank] = 1;
       need_dst[m.dst_rank] = 1;
     }
@@ -425,14 +435,14 @@ int coadapt_reshard_execute(coadapt_reshard_plan* p, int dst_rank,
       if (prev >= 0 && prev != dev) cudaSetDevice(prev);
     }
   } restore{prev, device};
-  auto& T = p->cache[{dst_rank, elem_bytes}];
+  auto& T = p->cache[{role, rank, elem_bytes}];
   if (T.dev && T.device != device)
     return fail(COADAPT_E_VALIDATION, "reshard: plan executed on another device");
   if (!T.dev && T.n == 0) {
     std::vector<CopyTask> tasks;
     int rc = guarded([&] {
       for (const auto& m : p->plan.moves)
-        if (dst_rank < 0 || m.dst_rank == dst_rank)
+        if (mine(m))
           emit_tasks(m, p->src.shards[m.src_shard], p->dst.shards[m.dst_shard],
                      elem_bytes, tasks);
       return COADAPT_OK;

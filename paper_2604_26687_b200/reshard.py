@@ -21,6 +21,7 @@ from . import _lib as L
 from ._lib import check, lib
 
 SRC, DST = 0, 1
+ROLE_ALL, ROLE_PULL, ROLE_PUSH = 0, 1, 2
 POLICIES = {"canonical": 0, "spread": 1}
 
 
@@ -180,12 +181,20 @@ class TransferPlan:
         return out.value
 
     # ------------------------------------------------------------- execute
-    def execute(self, src_packs: Sequence, dst_packs: Sequence, dst_rank: int = -1,
-                elem_bytes: Optional[int] = None, device: Optional[int] = None, stream=None) -> None:
-        """Pull every region into `dst_packs` (all destination ranks when
-        dst_rank == -1, else that rank only).  Packs are CUDA tensors or raw
-        device addresses (ints, e.g. IPC-mapped peers); None where unused."""
+    def execute(self, src_packs: Sequence, dst_packs: Sequence, dst_rank: Optional[int] = None,
+                src_rank: Optional[int] = None, elem_bytes: Optional[int] = None,
+                device: Optional[int] = None, stream=None) -> None:
+        """Copy the plan's regions for one state plane.  Default: every move
+        (all packs visible here).  ``dst_rank=r``: pull the moves into r
+        (this GPU reads local + peer sources); ``src_rank=r``: push the moves
+        out of r (this GPU writes local + peer destinations).  Packs are
+        CUDA tensors or raw device addresses (ints, e.g. IPC-mapped peers);
+        None where unused."""
         from .device import _ptr, _stream
+        if dst_rank is not None and src_rank is not None:
+            raise L.ValidationError("pass dst_rank (pull) or src_rank (push), not both")
+        role, rank = ((ROLE_PULL, dst_rank) if dst_rank is not None and dst_rank >= 0 else
+                      (ROLE_PUSH, src_rank) if src_rank is not None else (ROLE_ALL, -1))
         ns, nd = len(src_packs), len(dst_packs)
         sp = (C.c_void_p * max(1, ns))(*[None if x is None else _ptr(x) for x in src_packs])
         dp = (C.c_void_p * max(1, nd))(*[None if x is None else _ptr(x) for x in dst_packs])
@@ -195,7 +204,7 @@ class TransferPlan:
                 raise L.ValidationError("pass elem_bytes and device with raw pointers")
             elem_bytes = t.element_size() if elem_bytes is None else elem_bytes
             device = t.device.index if device is None else device
-        check(lib().coadapt_reshard_execute(self.handle, int(dst_rank), sp, ns, dp, nd,
+        check(lib().coadapt_reshard_execute(self.handle, role, int(rank), sp, ns, dp, nd,
                                             int(elem_bytes), int(device), _stream(stream)))
 
 

@@ -2,12 +2,15 @@
 launched with torch.distributed.run (one process per GPU, world = d*t*p of
 both layouts).
 
-Every rank fills its source pack from the deterministic global tensors,
-publishes a CUDA IPC handle, maps the peers' packs and pulls its destination
-pack with coadapt_reshard_execute(dst_rank = rank).  Checks (rank 0 prints
-one JSON line): every destination pack equals the oracle's pack built from
-the global tensors; and, for a larger TP -> PP transition, the pull
-bandwidth per GPU (wire bytes received / kernel time, CUDA events).
+Every rank fills its source pack from the deterministic global tensors and
+publishes a CUDA IPC handle; in pull mode it maps the peers' source packs
+and copies its destination pack (role PULL, rank = itself), in push mode it
+maps the peers' destination packs and writes its source regions into them
+(role PUSH).  Checks (rank 0 prints one JSON line): every destination pack
+equals the oracle's pack built from the global tensors, for every strategy
+pair of the world size, both modes; and, for a larger TP -> PP transition,
+the copy bandwidth per GPU (CUDA events) in both modes, with a round trip
+back to the source layout.
 """
 import json
 import os
@@ -50,7 +53,7 @@ def map_peers(rank, world, mine, local):
     return ptrs, bases
 
 
-def run_case(rank, world, local, m, a, b, dt, policy="canonical", timed=False):
+def run_case(rank, world, local, m, a, b, dt, policy="canonical", timed=False, mode="pull"):
     om = to_oracle(m)
     la, lb = O.layout_for(om, a), O.layout_for(om, b)
     p = R.plan_transfers(m, a, b, policy)
@@ -65,29 +68,42 @@ def run_case(rank, world, local, m, a, b, dt, policy="canonical", timed=False):
         src = torch.from_numpy(O.pack_from_global(la, rank, st, dt)).cuda()
         want = O.pack_from_global(lb, rank, st, dt)
     dst = torch.zeros(lb.pack_numel[rank], dtype=src.dtype, device="cuda")
-    ptrs, bases = map_peers(rank, world, src, local)
+
+    def go(plan, s_t, d_t, s_list, d_list):
+        if mode == "pull":
+            plan.execute(s_list, [d_t if r == rank else None for r in range(world)], dst_rank=rank)
+        else:
+            plan.execute([s_t if r == rank else None for r in range(world)], d_list, src_rank=rank)
+
+    # pull maps the peers' sources, push the peers' destinations
+    ptrs, bases = map_peers(rank, world, src if mode == "pull" else dst, local)
+    sl = ptrs if mode == "pull" else None
+    dl = ptrs if mode == "push" else None
     torch.cuda.synchronize()
     dist.barrier()
-    res = {}
+    res = {"mode": mode}
     if timed:
-        recv = sum(x.bytes for x in p.moves() if x.dst_rank == rank and not x.local)
-        wire = recv // m.bytes_per_element * es  # this plane's wire bytes
+        moves = p.moves()
+        mine = [x for x in moves if (x.dst_rank if mode == "pull" else x.src_rank) == rank]
+        wire = sum(x.bytes for x in mine if not x.local) // m.bytes_per_element * es
+        total = sum(x.bytes for x in mine) // m.bytes_per_element * es
         s = torch.cuda.current_stream()
         for _ in range(3):
-            p.execute(ptrs, [dst if r == rank else None for r in range(world)], dst_rank=rank)
+            go(p, src, dst, sl, dl)
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 10
         e0.record(s)
         for _ in range(reps):
-            p.execute(ptrs, [dst if r == rank else None for r in range(world)], dst_rank=rank)
+            go(p, src, dst, sl, dl)
         e1.record(s)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        res = {"ms": ms, "wire_bytes": wire, "pack_bytes": dst.numel() * es,
-               "wire_gbs": wire / ms / 1e6, "pack_gbs": dst.numel() * es / ms / 1e6}
-        # round trip back into a fresh source-layout pack and compare
+        res.update({"ms": ms, "wire_bytes": wire, "bytes": total,
+                    "wire_gbs": wire / ms / 1e6, "gbs": total / ms / 1e6})
+        dist.barrier()
+        # round trip back into a fresh source-layout pack (pulled) and compare
         back = R.plan_transfers(m, b, a, policy)
         dptrs, dbases = map_peers(rank, world, dst, local)
         again = torch.zeros_like(src)
@@ -104,8 +120,9 @@ def run_case(rank, world, local, m, a, b, dt, policy="canonical", timed=False):
         for x in dbases:
             D.ipc_close(x)
     else:
-        p.execute(ptrs, [dst if r == rank else None for r in range(world)], dst_rank=rank)
+        go(p, src, dst, sl, dl)
         torch.cuda.synchronize()
+        dist.barrier()  # push: peers write into this rank's dst
         res["ok"] = bool(np.array_equal(dst.cpu().numpy(), want))
     dist.barrier()
     for x in bases:
@@ -128,16 +145,19 @@ def main():
         for b in ss:
             for dt in (np.int16, np.float32):
                 pol = rng.choice(["canonical", "spread"])
-                r = run_case(rank, world, local, small, a, b, dt, pol)
-                cases.append({"src": a, "dst": b, "es": np.dtype(dt).itemsize, "ok": r["ok"]})
+                for mode in ("pull", "push"):
+                    r = run_case(rank, world, local, small, a, b, dt, pol, mode=mode)
+                    cases.append({"src": a, "dst": b, "es": np.dtype(dt).itemsize, "mode": mode,
+                                  "ok": r["ok"]})
     # bandwidth: TP across all GPUs -> PP across all GPUs (each rank pulls
     # (world-1)/world of its new stage from the peers)
     big = R.ModelSpec(world * 2, (T("w", (8192, 8192), 0), T("o", (8192, 8192), 1)))
-    timed = run_case(rank, world, local, big, (1, world, 1), (1, 1, world), np.int16, timed=True)
+    timed = [run_case(rank, world, local, big, (1, world, 1), (1, 1, world), np.int16, timed=True,
+                      mode=mode) for mode in ("pull", "push")]
     oks = [None] * world
     dist.all_gather_object(oks, (all(c["ok"] for c in cases), timed))
     if rank == 0:
-        ok = all(o[0] and o[1]["ok"] for o in oks)
+        ok = all(o[0] and all(t["ok"] for t in o[1]) for o in oks)
         print(json.dumps({"ok": ok, "world": world, "cases": len(cases),
                           "failed": [c for c in cases if not c["ok"]][:5],
                           "bandwidth": [o[1] for o in oks]}))

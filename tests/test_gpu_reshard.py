@@ -65,6 +65,13 @@ def test_execute_matches_oracle(es, misalign):
         torch.cuda.synchronize()
         for r in range(len(dst2)):
             assert torch.equal(dst2[r], dst[r])
+        # one source at a time (push)
+        dst3 = [upload(np.zeros(n, dt), misalign)[0] for n in lb.pack_numel]
+        for r in range(len(src)):
+            p.execute(src, dst3, src_rank=r)
+        torch.cuda.synchronize()
+        for r in range(len(dst3)):
+            assert torch.equal(dst3[r], dst[r])
 
 
 def test_execute_validation():
