@@ -4,9 +4,10 @@
 // no header): shard layouts for a (d,t,p) strategy, box-intersection
 // transfer plans, a latency model, and execution.  Names and semantics
 // follow SPEC.md; execution here is the B200 one — every destination rank
-// pulls its regions straight out of the source ranks' HBM (NVLink peer
-// loads through CUDA IPC pointers), one kernel per state plane, instead of
-// the paper's host-staged five-phase pipeline.
+// pulls its regions straight out of the source ranks' HBM (or every source
+// rank pushes into the destinations'), NVLink peer accesses through CUDA
+// IPC pointers, one kernel per state plane, instead of the paper's
+// host-staged five-phase pipeline.
 //
 // Layout rules (plus the choices SPEC leaves open):
 //   * ranks are numbered Megatron-style, tp fastest, then dp, then pp:
@@ -23,10 +24,13 @@
 #pragma once
 
 #include <cstdint>
+#include <span>
 #include <string>
 #include <vector>
 
 #include "coadapt/strategy.hpp"
+
+struct coadapt_reshard_plan;
 
 namespace coadapt::reshard {
 
@@ -130,5 +134,44 @@ double estimate_reconfig_latency(
 
 // "key,src_rank,dst_rank,offsets,extents,bytes,local".
 std::string transfer_plan_csv(const ModelSpec& model, const TransferPlan& plan);
+
+// The device executor (RAII over coadapt_reshard.h): both layouts, the
+// plan, and the copy-task tables it builds per (role, rank, element size).
+// pull(r): copy every move into destination rank r (sources: this GPU's
+// and NVLink peers' packs); push(r): every move out of source rank r;
+// all(): every move (all packs visible to this process).  Pack pointer
+// arrays are indexed by rank (nullptr where unused).  Throws
+// ValidationError / InternalError like the rest of the API.
+class DevicePlan {
+ public:
+  DevicePlan(const ModelSpec& model, const ParallelStrategy& src,
+             const ParallelStrategy& dst,
+             SourcePolicy policy = SourcePolicy::kCanonical);
+  ~DevicePlan();
+  DevicePlan(const DevicePlan&) = delete;
+  DevicePlan& operator=(const DevicePlan&) = delete;
+
+  const ShardLayout& source() const { return src_; }
+  const ShardLayout& destination() const { return dst_; }
+  const TransferPlan& plan() const { return plan_; }
+
+  void pull(int dst_rank, std::span<const void* const> src_packs,
+            std::span<void* const> dst_packs, int elem_bytes, int device,
+            void* stream);
+  void push(int src_rank, std::span<const void* const> src_packs,
+            std::span<void* const> dst_packs, int elem_bytes, int device,
+            void* stream);
+  void all(std::span<const void* const> src_packs,
+           std::span<void* const> dst_packs, int elem_bytes, int device,
+           void* stream);
+
+ private:
+  void run(int role, int rank, std::span<const void* const> src_packs,
+           std::span<void* const> dst_packs, int elem_bytes, int device,
+           void* stream);
+  ShardLayout src_, dst_;
+  TransferPlan plan_;
+  coadapt_reshard_plan* handle_ = nullptr;
+};
 
 }  // namespace coadapt::reshard
