@@ -22,10 +22,18 @@
  *    thread-local message of the last failure on the calling thread.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *    stream).  All device work is asynchronous on that stream; only
- *    coadapt_gns_result / coadapt_gns_read_partials block.
+ *    coadapt_gns_read_result / coadapt_gns_read_partials block.
  *  - device gradient buffers are borrowed (like std::span): the library never
- *    frees or retains them past the call's stream work.
- *  - one coadapt_gns per (device, stream); it is not thread-safe.
+ *    frees or retains them past the call's stream work.  Host buffers given
+ *    to coadapt_gns_fused_sqnorm_host must stay valid until that stream work
+ *    completes (pinned memory for the copies to overlap).
+ *  - one coadapt_gns per (device, stream); it is not thread-safe, and its
+ *    launches share scratch (per-CTA partials, a completion ticket), so all
+ *    calls on one coadapt_gns must be ordered on one stream (or streams
+ *    joined by events).  Plans are read-only after their first use and may
+ *    be shared; their first fused/accumulate use builds a chunk table
+ *    (synchronous), so make that first call before any CUDA-graph capture —
+ *    after it, begin_step .. finalize are capturable and replayable.
  */
 #ifndef COADAPT_CUDA_H
 #define COADAPT_CUDA_H

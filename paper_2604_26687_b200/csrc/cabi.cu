@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -128,7 +129,9 @@ struct coadapt_plan {
     std::vector<uint64_t> prefix;
     uint64_t* dev = nullptr;
   };
-  std::vector<std::pair<int, Chunks>> chunks;
+  // deque: references stay valid while other P values are added
+  std::deque<std::pair<int, Chunks>> chunks;
+  std::mutex mu;  // guards the lazily built tables (chunks, full)
   // whole-bucket table for the trainer form (weight-0 ranges and gaps
   // included, abs == cum); built lazily, not for DP-slice plans
   bool is_slice = false;
@@ -320,6 +323,7 @@ int launch_fused_window(coadapt_gns* g, const coadapt_plan* p,
 
 // chunk numbering of `p` for chunk size P (built on first use, synchronous)
 int plan_chunks(coadapt_plan* p, int P, const coadapt_plan::Chunks** out) {
+  std::lock_guard<std::mutex> lock(p->mu);
   for (auto& kv : p->chunks)
     if (kv.first == P) {
       *out = &kv.second;
@@ -335,8 +339,14 @@ int plan_chunks(coadapt_plan* p, int P, const coadapt_plan::Chunks** out) {
   }
   c.prefix.back() = acc;
   CU(cudaMalloc(&c.dev, sizeof(uint64_t) * c.prefix.size()));
-  CU(cudaMemcpy(c.dev, c.prefix.data(), sizeof(uint64_t) * c.prefix.size(),
-                cudaMemcpyHostToDevice));
+  const cudaError_t e = cudaMemcpy(c.dev, c.prefix.data(),
+                                   sizeof(uint64_t) * c.prefix.size(),
+                                   cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(c.dev);
+    return fail(COADAPT_E_CUDA, std::string("chunk table upload: ") +
+                                    cudaGetErrorString(e));
+  }
   p->chunks.emplace_back(P, std::move(c));
   *out = &p->chunks.back().second;
   return COADAPT_OK;
@@ -359,8 +369,10 @@ uint64_t chunks_before(const coadapt_plan* p, const coadapt_plan::Chunks* ch,
 
 // whole-bucket range table (every element exactly once; gaps weight 0)
 int plan_full(coadapt_plan* p) {
+  std::lock_guard<std::mutex> lock(p->mu);
   if (p->full || p->bucket_numel == 0) return COADAPT_OK;
   std::vector<Range>& f = p->full_host;
+  f.clear();
   uint64_t at = 0;
   auto push = [&](uint64_t b, uint64_t n, double w) {
     if (n == 0) return;
@@ -375,9 +387,16 @@ int plan_full(coadapt_plan* p) {
     at = s.offset + s.numel;
   }
   if (at < p->bucket_numel) push(at, p->bucket_numel - at, 0.0);
-  CU(cudaMalloc(&p->full, sizeof(Range) * f.size()));
-  CU(cudaMemcpy(p->full, f.data(), sizeof(Range) * f.size(),
-                cudaMemcpyHostToDevice));
+  Range* dev = nullptr;
+  CU(cudaMalloc(&dev, sizeof(Range) * f.size()));
+  const cudaError_t e = cudaMemcpy(dev, f.data(), sizeof(Range) * f.size(),
+                                   cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(dev);
+    return fail(COADAPT_E_CUDA, std::string("range table upload: ") +
+                                    cudaGetErrorString(e));
+  }
+  p->full = dev;
   return COADAPT_OK;
 }
 
