@@ -182,6 +182,17 @@ def cpu_oracle_rate(host_bufs, dtype_code, segs, seconds, nthreads):
     return nbytes * passes / el / 1e9, nbytes, passes, el
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -396,11 +407,15 @@ def run_ours(args):
     # -- e2e: the same step through the host-pointer entry point (pinned host
     #    buckets, H2D inside the timed region), bounded sample per bucket
     e2e = None
-    if not args.no_e2e and fused:
+    if not args.no_e2e:
         E = min(args.e2e_elems, numel)
         segs_e = [(o, min(n, E - o), w) for o, n, w in mine[0].segments if o < E]
         plan_e = D.BucketPlan(segs_e, E, dt, dev)
         host = [pool[m][:E].cpu().pin_memory() for m in range(M)]
+        if not fused:  # d > 1: this rank's DP slice of the synchronised mean
+            d_job = c["d"]
+            slice_e = D.BucketPlan(segs_e, E, dt, dev, slice_index=0, slice_count=d_job)
+            host_mean = mean[:E].cpu().pin_memory()
         ge = D.GnsDevice(1, M, B_g, dev)
         if ws > 1:
             uid = D.nccl_unique_id() if rank == 0 else bytes(128)
@@ -410,7 +425,12 @@ def run_ours(args):
 
         def estep():
             ge.begin_step(stream)
-            ge.fused_sqnorm_host(plan_e, host, stream)
+            if fused:
+                ge.fused_sqnorm_host(plan_e, host, stream)
+            else:
+                for m in range(M):
+                    ge.micro_sqnorm_host(plan_e, host[m], 0, m, stream)
+                ge.mean_sqnorm_host(slice_e, host_mean, stream)
             ge.allreduce(stream)
             ge.finalize(B_g * SEQ_LEN, stream)
             rr = ge.result()
@@ -432,13 +452,20 @@ def run_ours(args):
             tt = torch.tensor([ems], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
-        ebytes = plan_e.active_bytes * M * ws
+        ebytes = (plan_e.active_bytes * M + (0 if fused else slice_e.active_bytes)) * ws
+        h2d = E * es * M
+        if not fused:
+            lo_e, hi_e = D.dp_slice(E, d_job, 0)
+            h2d += (hi_e - lo_e) * es
+        entry = ("coadapt_gns_fused_sqnorm_host (H2D overlapped with the fused reduction)"
+                 if fused else "coadapt_gns_micro_sqnorm_host x M + coadapt_gns_mean_sqnorm_host "
+                               "of DP slice 0 (H2D overlapped with K1)")
         e2e = {"value": round(ebytes / (ems / 1e3) / 1e9, 3), "unit": UNIT,
-               "h2d_bytes_per_step": int(E * es * M), "d2h_bytes_per_step": int(
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(
                    __import__("ctypes").sizeof(L.GnsResult)),
                "sample": f"first {E} elements of each of the {M} micro-buckets per GPU, "
-                         "pinned host memory -> coadapt_gns_fused_sqnorm_host (H2D overlapped "
-                         "with the fused reduction) -> allreduce -> finalize -> phi D2H -> decide"}
+                         f"pinned host memory -> {entry} -> allreduce -> finalize -> phi D2H "
+                         "-> decide"}
         ge.close()
         del host
 
@@ -452,9 +479,18 @@ def run_ours(args):
         segs_c = [(o, min(n, E - o), w) for o, n, w in mine[0].segments if o < E]
         nth = host_threads()
         rate, nb, passes, el = cpu_oracle_rate(hb, dt, segs_c, args.cpu_seconds, nth)
+        # SURVEY 8(d) variant (i): the reference's sequential model, 1 thread,
+        # on a quarter of the sample
+        hb1 = [b[:E // 4] for b in hb]
+        segs_1 = [(o, min(n, E // 4 - o), w) for o, n, w in segs_c if o < E // 4]
+        r1, nb1, p1, el1 = cpu_oracle_rate(hb1, dt, segs_1, max(2.0, args.cpu_seconds / 4), 1)
         cpu = {"value": round(rate, 3), "unit": UNIT, "cores": nth, "kind": "port",
                "sample": f"oracle fused fp64 pass over the first {E} elements of the {M} "
-                         f"micro-buckets ({nb / 1e9:.2f} GB), {passes} passes in {el:.1f} s"}
+                         f"micro-buckets ({nb / 1e9:.2f} GB), {passes} passes in {el:.1f} s",
+               "single_thread": {"value": round(r1, 3), "unit": UNIT, "cores": 1,
+                                 "sample": f"same pass over the first {E // 4} elements, "
+                                           f"{p1} passes in {el1:.1f} s"},
+               "cpu": cpu_model()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws,

@@ -193,6 +193,17 @@ int coadapt_gns_mean_sqnorm(coadapt_gns* g, const coadapt_plan* plan,
 int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* plan,
                                   const void* const* host_buckets,
                                   int micro_count, void* stream);
+/* As coadapt_gns_micro_sqnorm / coadapt_gns_mean_sqnorm with the bucket (or
+ * the synchronised mean gradient) in HOST memory: only the plan's span of
+ * elements (a DP slice for slice plans) is streamed H2D, in whole-stage
+ * windows through g's staging ring, each reduced as it lands.  The host
+ * form of record_micro_batch's caller loop (gns.hpp:19-20) and of the d > 1
+ * mean read. */
+int coadapt_gns_micro_sqnorm_host(coadapt_gns* g, const coadapt_plan* plan,
+                                  const void* host_bucket, int dp_index,
+                                  int micro, void* stream);
+int coadapt_gns_mean_sqnorm_host(coadapt_gns* g, const coadapt_plan* plan,
+                                 const void* host_mean, void* stream);
 
 /* Trainer form.  The gradient-accumulation add a trainer
  * does anyway — Megatron's fp32 main_grad.add_(grad) — with the GNS norms

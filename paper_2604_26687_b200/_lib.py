@@ -191,6 +191,8 @@ SIGNATURES = {
     "coadapt_sqnorm_host": (I, [P, U64, I, I, P]),
     "coadapt_synth_fill": (I, [P, I, P, SZ, U64, U64, F, F, P]),
     "coadapt_synth_mean_fill": (I, [P, I, P, SZ, U64, U64, I64, F, F, P]),
+    "coadapt_gns_micro_sqnorm_host": (I, [P, P, P, I, I, P]),
+    "coadapt_gns_mean_sqnorm_host": (I, [P, P, P, P]),
     "coadapt_l2_flush": (I, [P, U64, P]),
     "coadapt_read_probe": (I, [P, U64, P, P]),
     # coadapt_host.h

@@ -447,6 +447,63 @@ coadapt_gns_state default_state() {
 
 std::mutex g_oneshot_mu;
 
+// The host-streaming staging ring: kStages stages of kMaxFusedM * kStageElems
+// elements (sized for 8-byte elements on first use is wasteful; it is sized
+// for this element size and grown never — every later caller must fit).
+int ensure_staging(coadapt_gns* g, int es) {
+  const size_t need = (size_t)kStages * coadapt::dev::kMaxFusedM * kStageElems * es;
+  if (!g->staging) {
+    CU(cudaMalloc(&g->staging, need));
+    g->staging_bytes = need;
+    CU(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < kStages; ++i) {
+      CU(cudaEventCreateWithFlags(&g->stage_free[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&g->stage_full[i], cudaEventDisableTiming));
+    }
+  } else if (g->staging_bytes < need) {
+    return fail(COADAPT_E_VALIDATION,
+                "host streaming: this gns's staging ring was sized for a "
+                "smaller element type");
+  }
+  return COADAPT_OK;
+}
+
+// K1 over a HOST bucket: the plan's span of absolute elements is streamed
+// through the staging ring in windows of one whole stage; each window is
+// reduced (batched K1, one job) as it lands, into `slot`.
+int stream_host_k1(coadapt_gns* g, const coadapt_plan* p, const void* host,
+                   int slot, cudaStream_t s) {
+  if (p->host.empty()) return COADAPT_OK;
+  const int es = esize(p->dtype);
+  if (int rc = ensure_staging(g, es)) return rc;
+  const uint64_t win = (uint64_t)coadapt::dev::kMaxFusedM * kStageElems;
+  const size_t stage_bytes = (size_t)win * es;
+  const uint64_t lo = p->host.front().abs_begin;
+  const uint64_t hi = p->host.back().abs_begin + p->host.back().len;
+  for (int i = 0; i < kStages; ++i) CU(cudaEventRecord(g->stage_free[i], s));
+  const uint64_t nwin = (hi - lo + win - 1) / win;
+  for (uint64_t c = 0; c < nwin; ++c) {
+    const uint64_t w0 = lo + c * win, w1 = std::min(hi, w0 + win);
+    const uint64_t cb = cum_at(p, w0), ce = cum_at(p, w1);
+    if (ce == cb) continue;  // only weight-0 data in this window
+    const int st = (int)(c % kStages);
+    char* stage = static_cast<char*>(g->staging) + (size_t)st * stage_bytes;
+    CU(cudaStreamWaitEvent(g->copy_stream, g->stage_free[st], 0));
+    CU(cudaMemcpyAsync(stage, static_cast<const char*>(host) + w0 * es,
+                       (w1 - w0) * es, cudaMemcpyHostToDevice, g->copy_stream));
+    CU(cudaEventRecord(g->stage_full[st], g->copy_stream));
+    CU(cudaStreamWaitEvent(s, g->stage_full[st], 0));
+    BatchArgs jobs;
+    std::memset(&jobs, 0, sizeof(jobs));
+    jobs.count = 1;
+    jobs.ptr[0] = stage - w0 * es;  // abs element x lives at stage + (x-w0)*es
+    jobs.slot[0] = slot;
+    if (int rc = launch_batch(g, p, jobs, Window{cb, ce}, s)) return rc;
+    CU(cudaEventRecord(g->stage_free[st], s));
+  }
+  return COADAPT_OK;
+}
+
 }  // namespace
 
 // ====================================================================== API
@@ -721,18 +778,7 @@ int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
   GUARD(g->device);
   const int es = esize(p->dtype);
   const size_t stage_stride = kStageElems * es;  // per bucket per stage
-  const size_t need = (size_t)kStages * coadapt::dev::kMaxFusedM * stage_stride;
-  if (!g->staging) {
-    CU(cudaMalloc(&g->staging, need));
-    g->staging_bytes = need;
-    CU(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
-    for (int i = 0; i < kStages; ++i) {
-      CU(cudaEventCreateWithFlags(&g->stage_free[i], cudaEventDisableTiming));
-      CU(cudaEventCreateWithFlags(&g->stage_full[i], cudaEventDisableTiming));
-    }
-  } else if (g->staging_bytes < need) {
-    return fail(COADAPT_E_INTERNAL, "staging ring smaller than required");
-  }
+  if (int rc = ensure_staging(g, es)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // the compute stream must be done with every stage before we overwrite it
   for (int i = 0; i < kStages; ++i) CU(cudaEventRecord(g->stage_free[i], s));
@@ -780,6 +826,35 @@ int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
     CU(cudaEventRecord(g->stage_free[st], s));
   }
   return COADAPT_OK;
+}
+
+int coadapt_gns_micro_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
+                                  const void* host_bucket, int dp_index,
+                                  int micro, void* stream) {
+  if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
+  if (p->device != g->device)
+    return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
+  if (p->dtype == COADAPT_FP64)
+    return fail(COADAPT_E_VALIDATION, "fp64 buckets are not supported here");
+  if (int rc = check_slot(g, dp_index, micro)) return rc;
+  if (!host_bucket && p->active)
+    return fail(COADAPT_E_VALIDATION, "host bucket is NULL");
+  GUARD(g->device);
+  return stream_host_k1(g, p, host_bucket, dp_index * g->M + micro,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int coadapt_gns_mean_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
+                                 const void* host_mean, void* stream) {
+  if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
+  if (p->device != g->device)
+    return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
+  if (p->dtype == COADAPT_FP64)
+    return fail(COADAPT_E_VALIDATION, "fp64 buckets are not supported here");
+  if (!host_mean && p->active)
+    return fail(COADAPT_E_VALIDATION, "host mean gradient is NULL");
+  GUARD(g->device);
+  return stream_host_k1(g, p, host_mean, g->N, static_cast<cudaStream_t>(stream));
 }
 
 int coadapt_gns_accumulate(coadapt_gns* g, const coadapt_plan* p,

@@ -30,6 +30,14 @@ def _ptr(x) -> int:
     return int(x)
 
 
+def _host_ptr(x) -> int:
+    if isinstance(x, torch.Tensor):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):
+        return x.ctypes.data
+    return int(x)
+
+
 def _stream(stream) -> Optional[int]:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -140,6 +148,16 @@ class GnsDevice:
         ptrs = (C.c_void_p * max(1, k))(*[_ptr(b) if isinstance(b, torch.Tensor) else b.ctypes.data
                                           for b in host_buckets])
         check(lib().coadapt_gns_fused_sqnorm_host(self.handle, plan.handle, ptrs, k, _stream(stream)))
+
+    def micro_sqnorm_host(self, plan: BucketPlan, host_bucket, dp_index: int, micro: int,
+                          stream=None) -> None:
+        """K1 over a host (ideally pinned) bucket, streamed H2D."""
+        check(lib().coadapt_gns_micro_sqnorm_host(self.handle, plan.handle, _host_ptr(host_bucket),
+                                                  int(dp_index), int(micro), _stream(stream)))
+
+    def mean_sqnorm_host(self, plan: BucketPlan, host_mean, stream=None) -> None:
+        check(lib().coadapt_gns_mean_sqnorm_host(self.handle, plan.handle, _host_ptr(host_mean),
+                                                 _stream(stream)))
 
     ACC_FIRST, ACC_LAST_MEAN = 1, 2
 

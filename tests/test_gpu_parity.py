@@ -270,10 +270,12 @@ def test_layout_invariance_and_dedup(D, L, Lay):
     assert np.allclose(gc.partials(), gd.partials(), rtol=1e-12, atol=0)
 
 
-def test_world_step_matches_oracle(D, L, Lay):
+@pytest.mark.parametrize("phi_true", [256.0, 4096.0])
+def test_world_step_matches_oracle(D, L, Lay, phi_true):
+    # nominal and stress (cancellation, SURVEY 8(d)/App. B.3) noise scales
     spec = Lay.tiny_model(layers=4, h=128, ffn=256, vocab=512, tied=False)
     d, t, p, M = 2, 2, 2, 4
-    unit = Lay.noise_unit_for(1024.0, 1)
+    unit = Lay.noise_unit_for(phi_true, 1)
     g, lays = _emulate_world(D, L, Lay, spec, d, t, p, M, 7, unit)
     tokens = d * M * 2048
     g.finalize(tokens)
@@ -452,3 +454,30 @@ def test_accumulate_validation(D, L):
         g.accumulate(sl, main, grad, 0, 0)  # slice plan
     with pytest.raises(L.ValidationError):
         g.accumulate(plan, main[1:], grad, 0, 0)  # misaligned main_grad
+
+
+@pytest.mark.parametrize("dtype", [0, 2])
+def test_host_streaming_k1_matches_device(D, L, dtype):
+    """micro_sqnorm_host / mean_sqnorm_host (HOST buckets streamed H2D in
+    whole-stage windows) equal the device-resident K1 — across window
+    boundaries, weight-0 gaps, a DP-slice plan and an unaligned tail."""
+    tdt = getattr(torch, TDT[dtype])
+    n = (300 << 20) + 12345 if dtype == 0 else (40 << 20) + 77  # > 1 window for bf16
+    segs = [(0, 70_001, 1.0), (70_001, 1 << 20, 0.0), (70_001 + (1 << 20), n - 70_001 - (1 << 20), 0.5)]
+    dev_b = torch.randn(n, device="cuda").to(tdt)
+    host_b = dev_b.cpu().pin_memory()
+    full = D.BucketPlan(segs, n, dtype, 0)
+    sl = D.BucketPlan(segs, n, dtype, 0, slice_index=1, slice_count=3)
+    ga, gb = D.GnsDevice(2, 2, 8, 0), D.GnsDevice(2, 2, 8, 0)
+    for g in (ga, gb):
+        g.begin_step()
+    ga.micro_sqnorm(full, dev_b, 1, 0)
+    ga.mean_sqnorm(sl, dev_b)
+    gb.micro_sqnorm_host(full, host_b, 1, 0)
+    gb.mean_sqnorm_host(sl, host_b)
+    a, b = ga.partials(), gb.partials()
+    assert a[2] > 0 and a[-1] > 0
+    assert np.allclose(a, b, rtol=1e-12, atol=0), (a, b)
+    # oracle on the same bytes
+    ref = O.sqnorm(_host_u(dev_b), dtype, segs)
+    assert _rel(b[2], ref) <= RTOL_NORM
