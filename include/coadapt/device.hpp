@@ -71,6 +71,15 @@ class GnsDevicePlan {
                     std::span<const void* const> buckets, void* stream);
   void record_mean_gradient(const BucketLayout& layout, const void* mean,
                             void* stream);
+  // The same three with the buckets in HOST memory (pinned for overlap),
+  // streamed H2D through the plan's staging ring; buffers must stay valid
+  // until the stream work completes.
+  void record_micro_bucket_host(const BucketLayout& layout, const void* bucket,
+                                int dp_index, int micro, void* stream);
+  void record_fused_host(const BucketLayout& layout,
+                         std::span<const void* const> buckets, void* stream);
+  void record_mean_gradient_host(const BucketLayout& layout, const void* mean,
+                                 void* stream);
   // Trainer form (§8 f1): main_grad (+)= grad (fp32) with s_m fused in; on
   // the last micro-batch of a d == 1 step also gbar^2 (mean_scale_sq * |main|^2).
   void accumulate(const BucketLayout& layout, float* main_grad,

@@ -128,6 +128,25 @@ void GnsDevicePlan::record_mean_gradient(const BucketLayout& layout,
   check(coadapt_gns_mean_sqnorm(g_, layout.handle(), mean, stream));
 }
 
+void GnsDevicePlan::record_micro_bucket_host(const BucketLayout& layout,
+                                             const void* bucket, int dp_index,
+                                             int micro, void* stream) {
+  check(coadapt_gns_micro_sqnorm_host(g_, layout.handle(), bucket, dp_index,
+                                      micro, stream));
+}
+
+void GnsDevicePlan::record_fused_host(const BucketLayout& layout,
+                                      std::span<const void* const> buckets,
+                                      void* stream) {
+  check(coadapt_gns_fused_sqnorm_host(g_, layout.handle(), buckets.data(),
+                                      (int)buckets.size(), stream));
+}
+
+void GnsDevicePlan::record_mean_gradient_host(const BucketLayout& layout,
+                                              const void* mean, void* stream) {
+  check(coadapt_gns_mean_sqnorm_host(g_, layout.handle(), mean, stream));
+}
+
 void GnsDevicePlan::accumulate(const BucketLayout& layout, float* main_grad,
                                const void* micro_grad, int dp_index, int micro,
                                bool first, bool last_mean, double mean_scale_sq,
