@@ -1174,17 +1174,30 @@ int coadapt_sqnorm_host(const void* v, uint64_t n, int dtype, int device,
   }
   if (!v) return fail(COADAPT_E_VALIDATION, "vector is NULL");
   GUARD(device);
+  // bounded device footprint whatever n is (the span overload's host vector
+  // may be larger than HBM): fixed 32 Mi-element chunks,
+  // chunk sums added in chunk order on the host in fp64
+  const int es = esize(dtype);
+  const uint64_t chunk = std::min<uint64_t>(n, 32ull << 20);
   void* d = nullptr;
-  const size_t bytes = (size_t)n * esize(dtype);
-  CU(cudaMalloc(&d, bytes));
-  cudaError_t e = cudaMemcpy(d, v, bytes, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) {
-    cudaFree(d);
-    return fail(COADAPT_E_CUDA, std::string("sqnorm_host copy: ") +
-                                    cudaGetErrorString(e));
+  CU(cudaMalloc(&d, (size_t)chunk * es));
+  double total = 0.0;
+  int rc = COADAPT_OK;
+  for (uint64_t b = 0; b < n && rc == COADAPT_OK; b += chunk) {
+    const uint64_t k = std::min(chunk, n - b);
+    const cudaError_t e = cudaMemcpy(d, static_cast<const char*>(v) + b * es,
+                                     (size_t)k * es, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      rc = fail(COADAPT_E_CUDA,
+                std::string("sqnorm_host copy: ") + cudaGetErrorString(e));
+      break;
+    }
+    double part = 0.0;
+    rc = coadapt_sqnorm_device(d, k, dtype, device, &part, nullptr);
+    total += part;
   }
-  const int rc = coadapt_sqnorm_device(d, n, dtype, device, out, nullptr);
   cudaFree(d);
+  if (rc == COADAPT_OK) *out = total;
   return rc;
 }
 

@@ -481,3 +481,16 @@ def test_host_streaming_k1_matches_device(D, L, dtype):
     # oracle on the same bytes
     ref = O.sqnorm(_host_u(dev_b), dtype, segs)
     assert _rel(b[2], ref) <= RTOL_NORM
+
+
+def test_span_overload_chunked_large_vector(D, L):
+    """finalize_step(acc, span) with a host vector larger than one 32 Mi
+    chunk: bounded device footprint, same value as the oracle's fp64 sum."""
+    from paper_2604_26687_b200 import gns as G
+    rng = np.random.default_rng(1)
+    v = rng.normal(size=(32 << 20) + (5 << 20) + 3)
+    acc = G.StepAccumulator(1, 4)
+    for x in (3.0, 5.0):
+        acc.record_micro_batch(x)
+    st = G.finalize_step(acc, v)
+    assert _rel(st.mean_grad_sq, O.sumsq_f64(v)) <= 1e-13
