@@ -254,6 +254,13 @@ int coadapt_nccl_unique_id(void* out, size_t len); /* len >= 128 */
 int coadapt_gns_attach_nccl(coadapt_gns* g, int nranks, int rank,
                             const void* unique_id, size_t len);
 int coadapt_gns_allreduce(coadapt_gns* g, void* stream);
+/* One host thread driving n GPUs (one coadapt_gns per device, in rank
+ * order): attach_nccl_all builds their communicators at once
+ * (ncclCommInitAll); allreduce_group issues every rank's all-reduce inside
+ * one ncclGroupStart/End so the single thread cannot deadlock. */
+int coadapt_gns_attach_nccl_all(coadapt_gns* const* gs, int n);
+int coadapt_gns_allreduce_group(coadapt_gns* const* gs, void* const* streams,
+                                int n);
 
 /* finalize_step + update_ema + gns on the device (gns.hpp:42-73), one
  * thread, IEEE-exact twin of the host formulas.  Copies the result to

@@ -1040,6 +1040,53 @@ int coadapt_gns_attach_nccl(coadapt_gns* g, int nranks, int rank,
   return COADAPT_OK;
 }
 
+int coadapt_gns_attach_nccl_all(coadapt_gns* const* gs, int n) {
+  if (!gs || n < 1) return fail(COADAPT_E_VALIDATION, "need n >= 1 gns handles");
+  std::vector<int> devs(n);
+  for (int i = 0; i < n; ++i) {
+    if (!gs[i]) return fail(COADAPT_E_VALIDATION, "gns handle is NULL");
+    devs[i] = gs[i]->device;
+    for (int j = 0; j < i; ++j)
+      if (devs[j] == devs[i])
+        return fail(COADAPT_E_VALIDATION, "one gns per device");
+  }
+  std::vector<ncclComm_t> comms(n, nullptr);
+  NC(ncclCommInitAll(comms.data(), n, devs.data()));
+  for (int i = 0; i < n; ++i) {
+    if (gs[i]->comm) ncclCommDestroy(gs[i]->comm);
+    gs[i]->comm = comms[i];
+    gs[i]->nranks = n;
+    gs[i]->rank = i;
+  }
+  return COADAPT_OK;
+}
+
+int coadapt_gns_allreduce_group(coadapt_gns* const* gs, void* const* streams,
+                                int n) {
+  if (!gs || !streams || n < 1)
+    return fail(COADAPT_E_VALIDATION, "need n >= 1 gns handles and streams");
+  for (int i = 0; i < n; ++i) {
+    if (!gs[i]) return fail(COADAPT_E_VALIDATION, "gns handle is NULL");
+    if (gs[i]->N != gs[0]->N)
+      return fail(COADAPT_E_VALIDATION, "all ranks need the same d*M");
+  }
+  if (n == 1 || !gs[0]->comm) return COADAPT_OK;
+  NC(ncclGroupStart());
+  for (int i = 0; i < n; ++i) {
+    const ncclResult_t r =
+        ncclAllReduce(gs[i]->slots, gs[i]->slots, (size_t)gs[i]->N + 1,
+                      ncclFloat64, ncclSum, gs[i]->comm,
+                      static_cast<cudaStream_t>(streams[i]));
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      return fail(COADAPT_E_NCCL, std::string("ncclAllReduce: ") +
+                                      ncclGetErrorString(r));
+    }
+  }
+  NC(ncclGroupEnd());
+  return COADAPT_OK;
+}
+
 int coadapt_gns_allreduce(coadapt_gns* g, void* stream) {
   if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
   if (!g->comm || g->nranks == 1) return COADAPT_OK;  // local sum only

@@ -231,6 +231,18 @@ class GnsDevice:
             pass
 
 
+def attach_nccl_all(gs: Sequence["GnsDevice"]) -> None:
+    """One process driving len(gs) GPUs (one GnsDevice per device, rank order)."""
+    arr = (C.c_void_p * len(gs))(*[g.handle.value for g in gs])
+    check(lib().coadapt_gns_attach_nccl_all(arr, len(gs)))
+
+
+def allreduce_group(gs: Sequence["GnsDevice"], streams: Sequence) -> None:
+    arr = (C.c_void_p * len(gs))(*[g.handle.value for g in gs])
+    sts = (C.c_void_p * len(gs))(*[_stream(s) for s in streams])
+    check(lib().coadapt_gns_allreduce_group(arr, sts, len(gs)))
+
+
 def ipc_handle(t: torch.Tensor) -> tuple:
     """(64-byte CUDA IPC handle of the allocation holding `t`, offset of
     t.data_ptr() inside it) — send both to the peer (ipc_open)."""

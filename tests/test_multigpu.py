@@ -150,3 +150,57 @@ def test_reshard_pull_over_nvlink():
     rep = json.loads(lines[-1])
     print(json.dumps(rep))
     assert rep["ok"], rep
+
+
+@pytest.mark.gpu
+def test_single_process_drives_all_gpus():
+    """One host thread, one GnsDevice per GPU: communicators from
+    ncclCommInitAll, the slot all-reduce as one NCCL group; every GPU's
+    result equals the one-GPU computation of the same world."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs (gpurun --gpus 2)")
+    from paper_2604_26687_b200 import _lib as L
+    from paper_2604_26687_b200 import device as D
+    from paper_2604_26687_b200 import dist as Dist
+    from paper_2604_26687_b200 import layout as Lay
+    spec = Lay.tiny_model(layers=4, h=256, ffn=512, vocab=1000)
+    d, t, p, M = 2, 2, 2, 2
+    lays = Lay.world_layouts(spec, d, t, p)
+    unit = Lay.noise_unit_for(256.0, 1)
+
+    def reduce_on(dev, g, ranks, stream):
+        with torch.cuda.device(dev):
+            for vr in ranks:
+                lay = lays[vr]
+                i_d = lay.coords[0]
+                plan = D.BucketPlan(lay.segments, lay.numel, L.BF16, dev)
+                b = torch.empty(lay.numel, dtype=torch.bfloat16, device=f"cuda:{dev}")
+                for m in range(M):
+                    D.synth_fill(b, lay.gen, 11, i_d * M + m, Lay.G0, unit, stream)
+                    g.micro_sqnorm(plan, b, i_d, m, stream)
+                D.synth_mean_fill(b, lay.gen, 11, 0, d * M, Lay.G0, unit, stream)
+                sl = D.BucketPlan(lay.segments, lay.numel, L.BF16, dev, slice_index=i_d, slice_count=d)
+                g.mean_sqnorm(sl, b, stream)
+                torch.cuda.synchronize(dev)
+
+    one = D.GnsDevice(d, M, d * M, 0)
+    s0 = torch.cuda.Stream(device=0)
+    one.begin_step(s0)
+    reduce_on(0, one, range(len(lays)), s0)
+    one.finalize(d * M * 2048, s0)
+    ref = one.result()
+    gs = [D.GnsDevice(d, M, d * M, dev) for dev in range(n)]
+    D.attach_nccl_all(gs)
+    streams = [torch.cuda.Stream(device=dev) for dev in range(n)]
+    for dev in range(n):
+        gs[dev].begin_step(streams[dev])
+        reduce_on(dev, gs[dev], Dist.block_map(len(lays), n, dev), streams[dev])
+    D.allreduce_group(gs, streams)
+    for dev in range(n):
+        gs[dev].finalize(d * M * 2048, streams[dev])
+    for dev in range(n):
+        r = gs[dev].result()
+        assert abs(r.b_simple - ref.b_simple) <= 1e-12 * abs(ref.b_simple)
+        assert np.allclose(gs[dev].partials(), one.partials(), rtol=1e-13, atol=0)
