@@ -12,7 +12,7 @@
 // is row-major, so the box is `rows` runs of `row_bytes` contiguous bytes at
 // fixed pitches.  Trailing axes that the box spans completely on both sides
 // fold into the run; axes outside the last two are enumerated on the host.
-// Runs are cut into tasks of <= 512 KiB so 148 SMs share the work evenly.
+// Runs are cut into tasks of <= 1 MiB so 148 SMs share the work evenly.
 // Each CTA copies whole tasks with the widest access (16/8/4/2/1 B) that the
 // two addresses, run length and pitches allow; 16-byte copies keep 4
 // loads in flight per thread before storing (enough bytes in flight to
@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -42,7 +43,13 @@ namespace {
 namespace R = coadapt::reshard;
 
 constexpr int kMaxRanks = 64;
-constexpr uint64_t kTaskBytes = 512u << 10;
+// Tuned on 2 x B200 (tools/reshard_sweep.sh, TP->PP of 537 MB per rank):
+// grid {4,8,16} x SMs, {4,8} 16-byte loads in flight, {256 KiB, 1 MiB}
+// tasks all land at 600-670 GB/s of wire bytes — the NVLink bound; 1 MiB
+// tasks, 4 loads in flight, 4 CTAs per SM is the balanced choice.
+constexpr uint64_t kTaskBytes = 1u << 20;
+constexpr int kGridPerSM = 4;
+constexpr int kLoadsInFlight = 4;
 
 struct CopyTask {
   uint64_t src_off, dst_off;      // bytes into the packs
@@ -58,13 +65,13 @@ struct ExecArgs {
   char* dst[kMaxRanks];
 };
 
-template <class T>
+template <class T, int U16>
 __device__ __forceinline__ void copy_rows(const char* __restrict__ s,
                                           char* __restrict__ d,
                                           const CopyTask& t) {
   const uint32_t per_row = t.row_bytes / sizeof(T);
   const uint32_t total = per_row * t.rows;
-  constexpr int U = sizeof(T) == 16 ? 4 : 2;
+  constexpr int U = sizeof(T) == 16 ? U16 : 2;
   for (uint32_t base = threadIdx.x; base < total; base += U * blockDim.x) {
     T v[U];
     uint32_t idx[U];
@@ -85,6 +92,7 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ s,
   }
 }
 
+template <int U16>
 __global__ void __launch_bounds__(256)
 reshard_copy_kernel(const __grid_constant__ ExecArgs a) {
   for (uint32_t i = blockIdx.x; i < a.n_tasks; i += gridDim.x) {
@@ -95,15 +103,15 @@ reshard_copy_kernel(const __grid_constant__ ExecArgs a) {
                           reinterpret_cast<uintptr_t>(d) | t.row_bytes |
                           (t.rows > 1 ? (t.src_pitch | t.dst_pitch) : 0);
     if ((bits & 15) == 0)
-      copy_rows<uint4>(s, d, t);
+      copy_rows<uint4, U16>(s, d, t);
     else if ((bits & 7) == 0)
-      copy_rows<uint2>(s, d, t);
+      copy_rows<uint2, U16>(s, d, t);
     else if ((bits & 3) == 0)
-      copy_rows<uint32_t>(s, d, t);
+      copy_rows<uint32_t, U16>(s, d, t);
     else if ((bits & 1) == 0)
-      copy_rows<uint16_t>(s, d, t);
+      copy_rows<uint16_t, U16>(s, d, t);
     else
-      copy_rows<uint8_t>(s, d, t);
+      copy_rows<uint8_t, U16>(s, d, t);
   }
 }
 
@@ -465,8 +473,9 @@ int coadapt_reshard_execute(coadapt_reshard_plan* p, int role, int rank,
   for (int r = 0; r < D; ++r) a.dst[r] = static_cast<char*>(dst_packs[r]);
   int sms = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  const int grid = (int)std::min<uint32_t>(T.n, (uint32_t)sms * 4);
-  reshard_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  const int grid = (int)std::min<uint32_t>(T.n, (uint32_t)sms * kGridPerSM);
+  reshard_copy_kernel<kLoadsInFlight>
+      <<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
   CU(cudaGetLastError());
   coadapt_capi::count_launch();
   return COADAPT_OK;
