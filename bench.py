@@ -327,7 +327,7 @@ def run_ours(args):
     # the batched K1 over the M buckets)
     launch_bytes = [pl.active_elements * es * M for pl in plans]
 
-    ev_pairs = []
+    ev_pairs, tail_pairs, decide_s = [], [], []
 
     def step(timed):
         g.begin_step(stream)
@@ -345,10 +345,20 @@ def run_ours(args):
                 ev_pairs.append((e0, e1, launch_bytes[i]))
             if not fused:
                 g.mean_sqnorm(slices[i], mean, stream)
+        if timed:
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
         g.allreduce(stream)
         g.finalize(B_g * SEQ_LEN, stream)
+        if timed:
+            f1.record(stream)
+            tail_pairs.append((f0, f1))
         r = g.result()  # phi -> host (waits for this step)
+        h0 = time.perf_counter()
         G.decide(cands, r.phi if r.phi_available else None, current, 1000.0, 900.0, reconfig_cost=40.0)
+        if timed:
+            decide_s.append(time.perf_counter() - h0)
         return r
 
     for _ in range(args.warmup):
@@ -388,6 +398,15 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     value = job_bytes / (ms / 1e3) / 1e9
+
+    # C5 "full goodput step" latency split: the reductions,
+    # the all-reduce + finalize tail on the device, the host decide()
+    red_ms = sum(a.elapsed_time(b) for a, b, _ in ev_pairs) / args.steps
+    tail_ms = sum(a.elapsed_time(b) for a, b in tail_pairs) / max(1, len(tail_pairs))
+    goodput_step = {"step_ms": round(ms, 4), "reductions_ms": round(red_ms, 4),
+                    "allreduce_finalize_ms": round(tail_ms, 4),
+                    "decide_ms": round(1e3 * sum(decide_s) / max(1, len(decide_s)), 4),
+                    "candidates": len(cands)}
 
     # dominant-kernel roofline (per-launch CUDA events on the launching stream)
     durs = [a.elapsed_time(b) / 1e3 for a, b, _ in ev_pairs]
@@ -505,6 +524,7 @@ def run_ours(args):
                            "pool": ("virtual ranks on one GPU share one resident set of M buckets"
                                     if R // ws > 1 else "one resident set of M buckets per rank")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "goodput_step": goodput_step,
                 "clocks": clk,
                 "result": {"phi": r.phi if r.phi_available else None, "b_simple": r.b_simple,
                            "signal": r.stats.signal, "noise": r.stats.noise}}
