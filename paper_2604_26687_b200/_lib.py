@@ -16,7 +16,8 @@ import re
 import torch  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libcoadapt_b200.so")
+# COADAPT_LIB_PATH: load an alternative build (kernel A/B experiments only)
+LIB_PATH = os.environ.get("COADAPT_LIB_PATH") or os.path.join(_HERE, "lib", "libcoadapt_b200.so")
 INCLUDE_DIR = os.path.join(os.path.dirname(_HERE), "include")
 
 OK, E_VALIDATION, E_INTERNAL, E_CUDA, E_NCCL = 0, 1, 2, 3, 4
