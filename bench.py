@@ -479,7 +479,32 @@ def run_ours(args):
         entry = ("coadapt_gns_fused_sqnorm_host (H2D overlapped with the fused reduction)"
                  if fused else "coadapt_gns_micro_sqnorm_host x M + coadapt_gns_mean_sqnorm_host "
                                "of DP slice 0 (H2D overlapped with K1)")
-        e2e = {"value": round(ebytes / (ems / 1e3) / 1e9, 3), "unit": UNIT,
+        # the e2e roofline: plain pinned H2D copy rate of this GPU's link,
+        # measured with the same buffers (all ranks copying at once)
+        hb0 = host[0]
+        dbuf = torch.empty_like(hb0, device="cuda")
+        with torch.cuda.stream(stream):
+            dbuf.copy_(hb0, non_blocking=True)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if ws > 1:
+                stream.synchronize()
+                dist.barrier()
+            c0.record(stream)
+            for _ in range(4):
+                dbuf.copy_(hb0, non_blocking=True)
+            c1.record(stream)
+        stream.synchronize()
+        h2d_gbs = 4 * hb0.numel() * hb0.element_size() / (c0.elapsed_time(c1) / 1e3) / 1e9
+        del dbuf
+        if ws > 1:
+            tt = torch.tensor([h2d_gbs], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt)  # aggregate over the GPUs
+            h2d_gbs = float(tt.item())
+        e2e_value = ebytes / (ems / 1e3) / 1e9
+        e2e = {"value": round(e2e_value, 3), "unit": UNIT,
+               "h2d_peak_gbs": round(h2d_gbs, 1),
+               # bytes actually copied per second (all GPUs) / the link rate
+               "frac_of_h2d_peak": round(h2d * ws / (ems / 1e3) / 1e9 / h2d_gbs, 4),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(
                    __import__("ctypes").sizeof(L.GnsResult)),
                "sample": f"first {E} elements of each of the {M} micro-buckets per GPU, "
