@@ -499,3 +499,72 @@ def test_span_overload_chunked_large_vector(D, L):
     exact = math.fsum((v * v).tolist())
     assert _rel(st.mean_grad_sq, exact) <= 1e-12
     assert _rel(O.sumsq_f64(v), exact) <= 1e-11
+
+
+def _random_segments(rng, numel):
+    """a random segment table: gaps, tiny and long ranges, weights 0/0.5/1/2"""
+    segs, at = [], int(rng.integers(0, 9))
+    while at < numel:
+        kind = rng.integers(0, 4)
+        n = int(rng.integers(1, 8)) if kind == 0 else int(rng.integers(8, 70_000))
+        n = min(n, numel - at)
+        segs.append((at, n, float(rng.choice([0.0, 0.5, 1.0, 1.0, 2.0]))))
+        at += n + (int(rng.integers(0, 40)) if rng.random() < 0.3 else 0)
+    return segs
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_randomized_layouts_k1_k1f_host(D, L, seed):
+    """Randomized segment tables, base offsets, dtypes and M through every
+    reduction entry point (K1, K1f TMA/LDG, K2 slice, host streaming)
+    against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    dtype = int(rng.choice([0, 0, 1, 2]))
+    M = int(rng.choice([2, 3, 5, 7, 8, 11, 16]))
+    numel = int(rng.integers(1, 400_000))
+    off = int(rng.choice([0, 0, 1, 3, 8]))
+    segs = _random_segments(rng, numel)
+    gen = [(0, numel, 0, numel, numel)]
+    unit = O.noise_unit_for(2 ** -10, 512.0, 1)
+    raws = [_dev_buf(D, numel, dtype, gen, seed, m, unit, offset_elems=off) for m in range(M)]
+    bufs = [v for _, v in raws]
+    hb = [_host_u(b) for b in bufs]
+    plan = D.BucketPlan(segs, numel, dtype, 0)
+    s_ref, ss_ref = O.fused_sqnorms(hb, dtype, segs, 4)
+    # K1 (batched) and K1f
+    g1, g2 = D.GnsDevice(1, M, M, 0), D.GnsDevice(1, M, M, 0)
+    g1.begin_step()
+    g1.micro_sqnorm_batched(plan, bufs, [0] * M, list(range(M)))
+    g2.begin_step()
+    g2.fused_sqnorm(plan, bufs)
+    p1, p2 = g1.partials(), g2.partials()
+    for m in range(M):
+        assert _rel(p1[m], s_ref[m]) <= RTOL_NORM, (seed, m)
+        assert _rel(p2[m], s_ref[m]) <= RTOL_NORM, (seed, m)
+    assert _rel(p2[M], ss_ref / (M * M)) <= RTOL_NORM
+    # host streaming: one bucket through K1, all through K1f
+    g3 = D.GnsDevice(1, M, M, 0)
+    g3.begin_step()
+    host = [b.cpu().pin_memory() for b in bufs]
+    g3.micro_sqnorm_host(plan, host[0], 0, 0)
+    p3 = g3.partials()
+    assert _rel(p3[0], s_ref[0]) <= RTOL_NORM
+    g4 = D.GnsDevice(1, M, M, 0)
+    g4.begin_step()
+    g4.fused_sqnorm_host(plan, host)
+    p4 = g4.partials()
+    for m in range(M):
+        assert _rel(p4[m], s_ref[m]) <= RTOL_NORM
+    assert _rel(p4[M], ss_ref / (M * M)) <= RTOL_NORM
+    # K2 over a random DP slice
+    d = int(rng.integers(2, 5))
+    i = int(rng.integers(0, d))
+    sl = D.BucketPlan(segs, numel, dtype, 0, slice_index=i, slice_count=d)
+    lo, hi = D.dp_slice(numel, d, i)
+    segs_sl = [(max(o, lo), min(o + k, hi) - max(o, lo), w) for o, k, w in segs
+               if max(o, lo) < min(o + k, hi)]
+    g5 = D.GnsDevice(d, M, M * d, 0)
+    g5.begin_step()
+    g5.mean_sqnorm(sl, bufs[0])
+    ref = O.sqnorm(hb[0], dtype, segs_sl)
+    assert _rel(g5.partials()[-1], ref) <= RTOL_NORM
