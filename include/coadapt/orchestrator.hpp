@@ -82,7 +82,17 @@ struct OrchestratorConfig {
 struct ClockState {
   double elapsed = 0.0;  // T_elapsed
   double useful = 0.0;   // T_useful
+  // observed reconfiguration latencies so far (record_reconfig)
+  double reconfig_total = 0.0;
+  std::int64_t reconfigs = 0;
 };
+
+// a finished Reconfigure took `observed_latency` seconds
+// (e.g. reshard::estimate or the measured device pull + process-group
+// rebuild).  T_elapsed advances, T_useful does not; cfg.reconfig_cost
+// becomes the mean of all observed latencies.  ValidationError if < 0.
+void record_reconfig(ClockState& clock, OrchestratorConfig& cfg,
+                     double observed_latency);
 
 enum class CommandKind { kNoOp, kScaleBS, kReconfigure };
 

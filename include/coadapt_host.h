@@ -93,6 +93,16 @@ int coadapt_rank_candidates(const coadapt_candidate* c, size_t n, double phi,
                             const coadapt_candidate* current, double t_elapsed,
                             double t_useful, const coadapt_orch_cfg* cfg,
                             int64_t* order);
+/* record_reconfig: elapsed += latency (useful unchanged),
+ * *reconfig_cost = mean of all observed latencies (total / count). */
+typedef struct coadapt_clock {
+  double elapsed;
+  double useful;
+  double reconfig_total;
+  int64_t reconfigs;
+} coadapt_clock;
+int coadapt_record_reconfig(coadapt_clock* clock, double* reconfig_cost,
+                            double observed_latency);
 int coadapt_decide(const coadapt_candidate* c, size_t n, int phi_available,
                    double phi, const coadapt_candidate* current,
                    double t_elapsed, double t_useful,

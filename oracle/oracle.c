@@ -397,6 +397,18 @@ static int tie_better(const orc_entry* a, const orc_entry* b,
   return a->micro_batch < b->micro_batch;
 }
 
+/* SPEC.md:377-385 */
+int orc_record_reconfig(double* elapsed, double* useful, double* total,
+                        int64_t* count, double* reconfig_cost, double latency) {
+  (void)useful; /* "useful does not" advance */
+  if (!(latency >= 0.0)) return 1;
+  *elapsed += latency;
+  *total += latency;
+  *count += 1;
+  *reconfig_cost = *total / (double)*count;
+  return 0;
+}
+
 int orc_decide(const orc_entry* c, size_t n, int phi_available, double phi,
                const orc_entry* cur, double t_elapsed, double t_useful,
                const orc_orch_cfg* cfg, orc_command* out) {

@@ -170,6 +170,12 @@ typedef struct {
   int32_t pad_;
 } orc_command;
 
+/* record_reconfig: T_elapsed += latency (T_useful does
+ * not move); c_reconfig = mean of all observed latencies.  Returns 1 for
+ * latency < 0 (validation), else 0. */
+int orc_record_reconfig(double* elapsed, double* useful, double* total,
+                        int64_t* count, double* reconfig_cost, double latency);
+
 /* decide, SPEC.md:361-375 / Alg. 2 PAPER.md:490-515.  Returns 0 ok, 1 on
  * validation error (empty candidates, current absent). */
 int orc_decide(const orc_entry* cands, size_t n, int phi_available,

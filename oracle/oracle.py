@@ -103,6 +103,7 @@ def lib() -> C.CDLL:
             "orc_synth_profile": (SZ, [P, SZ, P, SZ, P, SZ, I, D, D, D, P, SZ]),
             "orc_feasible_candidates": (SZ, [P, SZ, P, SZ]),
             "orc_decide": (I, [P, SZ, I, D, P, D, D, P, P]),
+            "orc_record_reconfig": (I, [P, P, P, P, P, D]),
             "orc_score_candidates": (None, [P, SZ, D, P, D, D, P, P]),
             "orc_synth_fill": (None, [P, I, P, SZ, U64, U64, C.c_float, C.c_float]),
             "orc_synth_mean_fill": (None, [P, I, P, SZ, U64, U64, I64, C.c_float, C.c_float]),
@@ -244,6 +245,16 @@ def decide(cands, phi, current: Entry, t_elapsed, t_useful, margin=0.10, max_gro
     if rc:
         raise OracleError("decide: validation error")
     return out
+
+
+def record_reconfig(elapsed, useful, total, count, reconfig_cost, latency):
+    """SPEC.md:377-385 -> (elapsed, useful, total, count, reconfig_cost)"""
+    e, u, t = C.c_double(elapsed), C.c_double(useful), C.c_double(total)
+    n, c = C.c_int64(count), C.c_double(reconfig_cost)
+    if lib().orc_record_reconfig(C.byref(e), C.byref(u), C.byref(t), C.byref(n), C.byref(c),
+                                 float(latency)):
+        raise OracleError("record_reconfig: latency must be >= 0")
+    return e.value, u.value, t.value, n.value, c.value
 
 
 def score_candidates(cands, phi, current, t_elapsed, t_useful, reconfig_cost=0.0, reference_batch=16.0):

@@ -145,6 +145,11 @@ class ReshardInfoC(C.Structure):
                 ("src_max_pack_numel", C.c_uint64), ("dst_max_pack_numel", C.c_uint64)]
 
 
+class ClockC(C.Structure):
+    _fields_ = [("elapsed", C.c_double), ("useful", C.c_double), ("reconfig_total", C.c_double),
+                ("reconfigs", C.c_int64)]
+
+
 class TraceRowC(C.Structure):
     _fields_ = [("step", C.c_int64), ("tokens", C.c_int64), ("signal_raw", C.c_double),
                 ("noise_raw", C.c_double), ("ema_signal", C.c_double), ("ema_noise", C.c_double),
@@ -222,6 +227,7 @@ SIGNATURES = {
     "coadapt_profile_save": (I, [C.c_char_p, P, SZ]),
     "coadapt_decision_audit_csv": (I, [P, SZ, P, SZ, P]),
     "coadapt_simulate_micro_gradients": (I, [P, P, U64, I64, I, U64, P]),
+    "coadapt_record_reconfig": (I, [P, P, D]),
     # coadapt_reshard.h
     "coadapt_reshard_plan_create": (I, [P, P, P, I, P]),
     "coadapt_reshard_plan_destroy": (I, [P]),

@@ -272,6 +272,23 @@ int coadapt_decide(const coadapt_candidate* c, size_t n, int phi_available,
   });
 }
 
+int coadapt_record_reconfig(coadapt_clock* clock, double* reconfig_cost,
+                            double observed_latency) {
+  return guarded([&] {
+    if (!clock || !reconfig_cost) throw coadapt::ValidationError("NULL argument");
+    coadapt::ClockState c{clock->elapsed, clock->useful, clock->reconfig_total,
+                          clock->reconfigs};
+    coadapt::OrchestratorConfig cfg;
+    cfg.reconfig_cost = *reconfig_cost;
+    coadapt::record_reconfig(c, cfg, observed_latency);
+    clock->elapsed = c.elapsed;
+    clock->useful = c.useful;
+    clock->reconfig_total = c.reconfig_total;
+    clock->reconfigs = c.reconfigs;
+    *reconfig_cost = cfg.reconfig_cost;
+  });
+}
+
 int coadapt_trace_csv(const coadapt_trace_row* rows, size_t n, char* buf,
                       size_t cap, size_t* needed) {
   return guarded([&] {

@@ -147,6 +147,16 @@ std::vector<std::size_t> rank_candidates(std::span<const Candidate> candidates,
   return idx;
 }
 
+void record_reconfig(ClockState& clock, OrchestratorConfig& cfg,
+                     double observed_latency) {
+  if (!(observed_latency >= 0.0))
+    throw ValidationError("record_reconfig: latency must be >= 0");
+  clock.elapsed += observed_latency;
+  clock.reconfig_total += observed_latency;
+  clock.reconfigs += 1;
+  cfg.reconfig_cost = clock.reconfig_total / (double)clock.reconfigs;
+}
+
 Command decide(std::span<const Candidate> candidates, std::optional<double> phi,
                const ConfigTuple& current, const ClockState& clock,
                const OrchestratorConfig& cfg,

@@ -235,6 +235,27 @@ def rank_candidates(cands: Sequence[Candidate], phi: float, current: Candidate, 
     return out.tolist()
 
 
+@dataclass
+class ClockState:
+    """T_elapsed / T_useful + the observed reconfiguration
+    latencies record_reconfig averages into c_reconfig."""
+    elapsed: float = 0.0
+    useful: float = 0.0
+    reconfig_total: float = 0.0
+    reconfigs: int = 0
+
+
+def record_reconfig(clock: ClockState, observed_latency: float, reconfig_cost: float = 0.0) -> float:
+    """advance clock.elapsed by the latency (useful stays),
+    return the new c_reconfig = mean of all observed latencies."""
+    c = L.ClockC(clock.elapsed, clock.useful, clock.reconfig_total, clock.reconfigs)
+    cost = C.c_double(reconfig_cost)
+    check(lib().coadapt_record_reconfig(C.byref(c), C.byref(cost), float(observed_latency)))
+    clock.elapsed, clock.useful = c.elapsed, c.useful
+    clock.reconfig_total, clock.reconfigs = c.reconfig_total, c.reconfigs
+    return cost.value
+
+
 def decide(cands: Sequence[Candidate], phi: Optional[float], current: Candidate, t_elapsed: float,
            t_useful: float, margin: float = 0.10, max_growth: float = 2.0, reconfig_cost: float = 0.0,
            reference_batch: float = 16.0) -> Command:

@@ -236,3 +236,27 @@ def test_layout_generator_covers_every_parameter_once():
                 j = np.arange(n)
                 seen[base + (j // rl) * rs + (j % rl)] += 1
         assert (seen == 1).all(), (d, t, p)
+
+
+def test_record_reconfig_spec_examples(G):
+    """SPEC.md:377-385, through the C++ API (C-ABI) and the oracle."""
+    from oracle import oracle as O
+    clock = G.ClockState(elapsed=600.0, useful=600.0)
+    cost = G.record_reconfig(clock, 50.0, reconfig_cost=40.0)
+    assert (clock.useful, clock.elapsed) == (600.0, 650.0) and cost == 50.0
+    clock = G.ClockState()
+    G.record_reconfig(clock, 30.0)
+    assert G.record_reconfig(clock, 56.0) == 43.0
+    clock = G.ClockState(elapsed=10.0, useful=8.0)
+    cost = G.record_reconfig(clock, 0.0, reconfig_cost=40.0)
+    assert (clock.elapsed, clock.useful) == (10.0, 8.0) and cost == 0.0
+    with pytest.raises(G.ValidationError):
+        G.record_reconfig(clock, -1.0)
+    # random sequences agree with the oracle bit for bit
+    rng = np.random.default_rng(3)
+    c, o = G.ClockState(5.0, 4.0), (5.0, 4.0, 0.0, 0, 7.0)
+    cost = 7.0
+    for lat in rng.uniform(0, 90, 50):
+        cost = G.record_reconfig(c, lat, cost)
+        o = O.record_reconfig(*o, lat)
+        assert (c.elapsed, c.useful, c.reconfig_total, c.reconfigs, cost) == o
