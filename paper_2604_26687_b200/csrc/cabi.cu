@@ -887,8 +887,9 @@ int coadapt_gns_accumulate(coadapt_gns* g, const coadapt_plan* p,
   coadapt_plan* pm = const_cast<coadapt_plan*>(p);
   if (int rc = plan_full(pm)) return rc;
   if (p->bucket_numel == 0) return COADAPT_OK;
-  const int grid = grid_for(g->device, coadapt::dev::occupancy_accum(p->dtype),
-                            p->bucket_numel);
+  const int grid = grid_for(
+      g->device, coadapt::dev::occupancy_accum(p->dtype, flags & COADAPT_ACC_FIRST),
+      p->bucket_numel);
   if (int rc = ensure_partials(g, (size_t)grid * 2)) return rc;
   Sink sink{g->partials, g->ticket, g->slots};
   coadapt::dev::AccumArgs a{main_grad, micro_grad, flags,

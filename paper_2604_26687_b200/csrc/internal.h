@@ -79,7 +79,7 @@ struct AccumArgs {
   int32_t slot, gslot;
   double gscale;
 };
-int occupancy_accum(int dtype);
+int occupancy_accum(int dtype, bool first);
 cudaError_t launch_accum(int dtype, const Range* full, int nfull, uint64_t numel,
                          const AccumArgs& a, Sink sink, int grid, cudaStream_t s);
 

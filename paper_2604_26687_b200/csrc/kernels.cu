@@ -741,7 +741,7 @@ __device__ __forceinline__ void accum_elem(float* mg, float g, double w,
   }
 }
 
-template <int DT, int NT, int U>
+template <int DT, int NT, int U, bool FIRST>
 __global__ void __launch_bounds__(NT, 3)
     accum_kernel(const Range* __restrict__ R, int nr, uint64_t numel,
                  float* __restrict__ mg, const void* __restrict__ gp, int flags,
@@ -750,7 +750,10 @@ __global__ void __launch_bounds__(NT, 3)
   constexpr int ES = Elem<DT>::kSize, PV = Elem<DT>::kPerVec;
   constexpr uint64_t CE = (uint64_t)U * NT * PV;  // elements per chunk
   __shared__ double red[32];
-  const bool first = flags & 1, mean = flags & 2;
+  // the first micro-batch only reads the gradient (main_grad is written,
+  // not read): its own instantiation keeps twice the loads in flight
+  constexpr bool first = FIRST;
+  const bool mean = flags & 2;
   const uint64_t nchunks = (numel + CE - 1) / CE;
   double s = 0.0, gm = 0.0;
   int k = 0;
@@ -1359,18 +1362,26 @@ cudaError_t launch_fused(int dtype, int M, const Range* ranges, int nranges,
 }
 
 namespace {
-constexpr int kNTA = 256, kUA = 4;
-void* accum_fn(int dtype) {
+constexpr int kNTA = 256, kUA = 4, kUA1 = 8;  // kUA1: first micro-batch
+void* accum_fn(int dtype, bool first) {
   switch (dtype) {
-    case COADAPT_BF16: return reinterpret_cast<void*>(&accum_kernel<COADAPT_BF16, kNTA, kUA>);
-    case COADAPT_FP16: return reinterpret_cast<void*>(&accum_kernel<COADAPT_FP16, kNTA, kUA>);
-    case COADAPT_FP32: return reinterpret_cast<void*>(&accum_kernel<COADAPT_FP32, kNTA, kUA>);
+    case COADAPT_BF16:
+      return first ? reinterpret_cast<void*>(&accum_kernel<COADAPT_BF16, kNTA, kUA1, true>)
+                   : reinterpret_cast<void*>(&accum_kernel<COADAPT_BF16, kNTA, kUA, false>);
+    case COADAPT_FP16:
+      return first ? reinterpret_cast<void*>(&accum_kernel<COADAPT_FP16, kNTA, kUA1, true>)
+                   : reinterpret_cast<void*>(&accum_kernel<COADAPT_FP16, kNTA, kUA, false>);
+    case COADAPT_FP32:
+      return first ? reinterpret_cast<void*>(&accum_kernel<COADAPT_FP32, kNTA, kUA1, true>)
+                   : reinterpret_cast<void*>(&accum_kernel<COADAPT_FP32, kNTA, kUA, false>);
   }
   return nullptr;
 }
 }  // namespace
 
-int occupancy_accum(int dtype) { return occupancy_of(accum_fn(dtype), kNTA); }
+int occupancy_accum(int dtype, bool first) {
+  return occupancy_of(accum_fn(dtype, first), kNTA);
+}
 
 namespace {
 constexpr int kNTR = 256, kUR = 2;
@@ -1399,7 +1410,7 @@ cudaError_t launch_rs(int dtype, const Range* full, int nfull, uint64_t lo,
 cudaError_t launch_accum(int dtype, const Range* full, int nfull, uint64_t numel,
                          const AccumArgs& a, Sink sink, int grid,
                          cudaStream_t s) {
-  void* fn = accum_fn(dtype);
+  void* fn = accum_fn(dtype, a.flags & 1);
   if (!fn) return cudaErrorInvalidValue;
   float* mg = a.main_grad;
   const void* g = a.grad;
