@@ -788,8 +788,11 @@ __global__ void __launch_bounds__(NT, 3)
       const uint64_t nv = (A1 - A0) / PV;
       const uint4* gv = reinterpret_cast<const uint4*>(gb + A0 * ES);
       uint4* mv = reinterpret_cast<uint4*>(mg + A0);  // PV floats = PV/4 uint4
-      for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)U * NT) {
-        uint4 gr[U], mr[U][PV / 4];
+      // two register sets, software-pipelined: the loads of the next set
+      // are in flight while this one is converted, reduced and stored (the
+      // unpipelined loop drained the memory pipe every iteration: ncu
+      // long-scoreboard bound)
+      auto load_set = [&](uint64_t v0, uint4(&gr)[U], uint4(&mr)[U][PV / 4]) {
 #pragma unroll
         for (int j = 0; j < U; ++j) {
           const uint64_t v = v0 + (uint64_t)j * NT;
@@ -800,6 +803,8 @@ __global__ void __launch_bounds__(NT, 3)
               mr[j][h] = first ? make_uint4(0u, 0u, 0u, 0u) : ld_rw(mv + v * (PV / 4) + h);
           }
         }
+      };
+      auto process_set = [&](uint64_t v0, uint4(&gr)[U], uint4(&mr)[U][PV / 4]) {
 #pragma unroll
         for (int j = 0; j < U; ++j) {
           const uint64_t v = v0 + (uint64_t)j * NT;
@@ -826,6 +831,19 @@ __global__ void __launch_bounds__(NT, 3)
             if (mean) gm = fma(w, m0 + m1, gm);
           }
         }
+      };
+      constexpr uint64_t kStep = (uint64_t)U * NT;
+      uint4 gx[U], mx[U][PV / 4], gy[U], my[U][PV / 4];
+      uint64_t v0 = threadIdx.x;
+      if (v0 < nv) load_set(v0, gx, mx);
+      while (v0 < nv) {
+        if (v0 + kStep < nv) load_set(v0 + kStep, gy, my);
+        process_set(v0, gx, mx);
+        v0 += kStep;
+        if (v0 >= nv) break;
+        if (v0 + kStep < nv) load_set(v0 + kStep, gx, mx);
+        process_set(v0, gy, my);
+        v0 += kStep;
       }
     }
   }
@@ -1362,7 +1380,10 @@ cudaError_t launch_fused(int dtype, int M, const Range* ranges, int nranges,
 }
 
 namespace {
-constexpr int kNTA = 256, kUA = 4, kUA1 = 8;  // kUA1: first micro-batch
+// vectors per register set (two sets in flight); measured on 1 x B200, 1 Gi
+// bf16: (2, 4) 5.93 / 4.70 TB/s (add / first); (3, 6) 5.65 / 4.81;
+// (4, 4) 4.71 / 4.76 (spills); unpipelined (4, 8) 5.73 / 4.76
+constexpr int kNTA = 256, kUA = 2, kUA1 = 4;  // kUA1: first micro-batch
 void* accum_fn(int dtype, bool first) {
   switch (dtype) {
     case COADAPT_BF16:
