@@ -24,8 +24,9 @@ for m in range(M):
     bufs.append(b[:numel])
 host = [b.cpu().pin_memory() for b in bufs]
 plan = D.BucketPlan(segs, numel, L.BF16, 0)
-ref = None
+ref = {}
 bad = {"dev": 0, "host": 0}
+cross = 0.0
 for r in range(reps):
     for kind in ("dev", "host"):
         g = D.GnsDevice(1, M, M, 0)
@@ -35,10 +36,15 @@ for r in range(reps):
         else:
             g.fused_sqnorm_host(plan, host)
         p = g.partials()
-        if ref is None:
-            ref = p
-        elif not np.array_equal(p, ref):
+        # each path must be bit-reproducible run to run; the two paths sum
+        # in different window orders, so they agree to rounding only
+        if kind not in ref:
+            ref[kind] = p
+        elif not np.array_equal(p, ref[kind]):
             bad[kind] += 1
-            print(kind, r, "max rel", float(np.max(np.abs(p - ref) / np.abs(ref))), flush=True)
+            print(kind, r, "max rel", float(np.max(np.abs(p - ref[kind]) / np.abs(ref[kind]))),
+                  flush=True)
+        if len(ref) == 2:
+            cross = max(cross, float(np.max(np.abs(ref["host"] - ref["dev"]) / np.abs(ref["dev"]))))
         g.close()
-print("summary", bad, flush=True)
+print("summary", bad, "max rel host vs dev", cross, flush=True)
