@@ -262,6 +262,25 @@ int coadapt_gns_attach_nccl_all(coadapt_gns* const* gs, int n);
 int coadapt_gns_allreduce_group(coadapt_gns* const* gs, void* const* streams,
                                 int n);
 
+/* The all-reduce and the finalize as ONE kernel over NVLink peer memory
+ * (no NCCL launch on the step's tail): every rank pushes its N+1 slots into
+ * every rank's mailbox, raises a flag, waits for all ranks' flags, sums the
+ * blocks in rank order (bit-identical on every rank) and runs the finalize.
+ *   coadapt_gns_mailbox        allocate this rank's mailbox for nranks
+ *                              (share it with coadapt_ipc_handle)
+ *   coadapt_gns_attach_mailboxes  peers[q] = rank q's mailbox mapped here
+ *                              (coadapt_ipc_open; peers[rank] = own)
+ *   coadapt_gns_allreduce_finalize_p2p  replaces allreduce + finalize; every
+ *                              rank must call it once per step.  A peer
+ *                              that does not arrive within 10 s makes
+ *                              coadapt_gns_read_result fail with status 2.
+ * Up to 8 ranks (one NVSwitch domain). */
+int coadapt_gns_mailbox(coadapt_gns* g, int nranks, void** mailbox);
+int coadapt_gns_attach_mailboxes(coadapt_gns* g, int nranks, int rank,
+                                 const void* const* peers);
+int coadapt_gns_allreduce_finalize_p2p(coadapt_gns* g, int64_t tokens,
+                                       void* stream);
+
 /* finalize_step + update_ema + gns on the device (gns.hpp:42-73), one
  * thread, IEEE-exact twin of the host formulas.  Copies the result to
  * pinned host memory on `stream`.  Replaces: finalize_step(acc, double)

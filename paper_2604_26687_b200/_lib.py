@@ -199,6 +199,9 @@ SIGNATURES = {
     "coadapt_synth_mean_fill": (I, [P, I, P, SZ, U64, U64, I64, F, F, P]),
     "coadapt_gns_micro_sqnorm_host": (I, [P, P, P, I, I, P]),
     "coadapt_gns_attach_nccl_all": (I, [P, I]),
+    "coadapt_gns_mailbox": (I, [P, I, P]),
+    "coadapt_gns_attach_mailboxes": (I, [P, I, I, P]),
+    "coadapt_gns_allreduce_finalize_p2p": (I, [P, I64, P]),
     "coadapt_gns_allreduce_group": (I, [P, P, I]),
     "coadapt_gns_mean_sqnorm_host": (I, [P, P, P, P]),
     "coadapt_l2_flush": (I, [P, U64, P]),

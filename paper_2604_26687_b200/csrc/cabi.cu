@@ -158,6 +158,11 @@ struct coadapt_gns {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   double* barrier_buf = nullptr;  // coadapt_gns_barrier scratch
+  // NVLink slot exchange (coadapt_gns_allreduce_finalize_p2p)
+  void* mbox = nullptr;
+  int mbox_world = 0, mbox_cap = 0, mbox_rank = -1;
+  char* mbox_peers[coadapt::dev::kMaxPeers] = {};
+  uint64_t epoch = 0;
   // host streaming (coadapt_gns_fused_sqnorm_host)
   void* staging = nullptr;  // kStages * 16 * kStageElems * es bytes
   size_t staging_bytes = 0;
@@ -623,6 +628,7 @@ int coadapt_gns_destroy(coadapt_gns* g) {
     cudaDeviceSynchronize();
     if (g->comm) ncclCommDestroy(g->comm);
     if (g->barrier_buf) cudaFree(g->barrier_buf);
+    if (g->mbox) cudaFree(g->mbox);
     if (g->slots) cudaFree(g->slots);
     if (g->partials) cudaFree(g->partials);
     if (g->ticket) cudaFree(g->ticket);
@@ -1097,6 +1103,84 @@ int coadapt_gns_allreduce(coadapt_gns* g, void* stream) {
   return COADAPT_OK;
 }
 
+int coadapt_gns_mailbox(coadapt_gns* g, int nranks, void** out) {
+  if (!g || !out) return fail(COADAPT_E_VALIDATION, "gns/out is NULL");
+  if (nranks < 1 || nranks > coadapt::dev::kMaxPeers)
+    return fail(COADAPT_E_VALIDATION, "mailbox: 1 <= nranks <= 8");
+  GUARD(g->device);
+  const int cap = std::max(g->slot_cap, g->N + 1);
+  if (!g->mbox || g->mbox_world != nranks || g->mbox_cap < cap) {
+    if (g->mbox) {
+      CU(cudaDeviceSynchronize());
+      cudaFree(g->mbox);
+      g->mbox = nullptr;
+    }
+    const size_t bytes = coadapt::dev::mailbox_bytes(nranks, cap);
+    CU(cudaMalloc(&g->mbox, bytes));
+    CU(cudaMemset(g->mbox, 0, bytes));
+    g->mbox_world = nranks;
+    g->mbox_cap = cap;
+    g->mbox_rank = -1;
+    g->epoch = 0;
+  }
+  *out = g->mbox;
+  return COADAPT_OK;
+}
+
+int coadapt_gns_attach_mailboxes(coadapt_gns* g, int nranks, int rank,
+                                 const void* const* peers) {
+  if (!g || !peers) return fail(COADAPT_E_VALIDATION, "gns/peers is NULL");
+  if (!g->mbox || nranks != g->mbox_world)
+    return fail(COADAPT_E_VALIDATION,
+                "call coadapt_gns_mailbox(g, nranks) first, with the same nranks");
+  if (rank < 0 || rank >= nranks)
+    return fail(COADAPT_E_VALIDATION, "rank out of range");
+  for (int q = 0; q < nranks; ++q) {
+    if (!peers[q]) return fail(COADAPT_E_VALIDATION, "peer mailbox is NULL");
+    g->mbox_peers[q] = static_cast<char*>(const_cast<void*>(peers[q]));
+  }
+  if (g->mbox_peers[rank] != g->mbox)
+    return fail(COADAPT_E_VALIDATION, "peers[rank] must be this gns's own mailbox");
+  g->mbox_rank = rank;
+  return COADAPT_OK;
+}
+
+int coadapt_gns_allreduce_finalize_p2p(coadapt_gns* g, int64_t tokens,
+                                       void* stream) {
+  if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
+  if (tokens < 0) return fail(COADAPT_E_VALIDATION, "tokens must be >= 0");
+  if (g->mbox_rank < 0)
+    return fail(COADAPT_E_VALIDATION, "no mailboxes attached");
+  if (g->N + 1 > g->mbox_cap)
+    return fail(COADAPT_E_VALIDATION,
+                "d*M grew past the mailbox capacity: recreate the mailboxes");
+  GUARD(g->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  coadapt::dev::P2PArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.fin = coadapt::dev::FinalizeArgs{g->slots, g->N, g->global_batch, tokens,
+                                     g->state, g->result};
+  a.slots = g->slots;
+  a.world = g->mbox_world;
+  a.rank = g->mbox_rank;
+  a.cap = g->mbox_cap;
+  a.epoch = ++g->epoch;
+  a.timeout_ns = 10'000'000'000ll;  // a peer 10 s late is a failure, not a hang
+  for (int q = 0; q < a.world; ++q) a.mbox[q] = g->mbox_peers[q];
+  CU(coadapt::dev::launch_p2p_finalize(a, s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CU(cudaMemcpyAsync(g->result_host, g->result, sizeof(coadapt_gns_result),
+                     cudaMemcpyDeviceToHost, s));
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(s, &cap));
+  if (cap == cudaStreamCaptureStatusActive)
+    CU(cudaEventRecordWithFlags(g->result_ready, s, cudaEventRecordExternal));
+  else
+    CU(cudaEventRecord(g->result_ready, s));
+  g->finalized = true;
+  return COADAPT_OK;
+}
+
 int coadapt_gns_finalize(coadapt_gns* g, int64_t tokens, void* stream) {
   if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
   if (tokens < 0) return fail(COADAPT_E_VALIDATION, "tokens must be >= 0");
@@ -1128,6 +1212,10 @@ int coadapt_gns_read_result(coadapt_gns* g, coadapt_gns_result* out) {
   GUARD(g->device);
   CU(cudaEventSynchronize(g->result_ready));
   *out = *g->result_host;
+  if (out->status == COADAPT_E_INTERNAL)
+    return fail(COADAPT_E_INTERNAL,
+                "NVLink slot exchange timed out waiting for a peer "
+                "(coadapt_gns_allreduce_finalize_p2p); GnsState left unchanged");
   if (out->status != COADAPT_OK)
     return fail(COADAPT_E_VALIDATION,
                 "a squared-norm partial was negative or non-finite "

@@ -1033,8 +1033,7 @@ static_assert(sizeof(DevResult) == sizeof(coadapt_gns_result), "layout");
 // Single thread, explicit round-to-nearest intrinsics: no FMA contraction,
 // so every value is bit-identical to the host C++ formulas
 // (gns.hpp:42-44, 64-66, 70-72).
-__global__ void finalize_kernel(FinalizeArgs a) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void finalize_body(const FinalizeArgs& a) {
   DevState* st = static_cast<DevState*>(a.state);
   DevResult* res = static_cast<DevResult*>(a.result);
   const int n = a.n;
@@ -1097,6 +1096,89 @@ __global__ void finalize_kernel(FinalizeArgs a) {
     res->phi = __longlong_as_double(0x7ff8000000000000ll);
     res->phi_available = 0;
   }
+}
+
+__global__ void finalize_kernel(FinalizeArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  finalize_body(a);
+}
+
+// ---------------------------------------------------------------- X1+K3 P2P
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One CTA.  Blocks are double-buffered by epoch parity: a rank can be at
+// most one epoch ahead of any reader (it needs every rank's flag of the
+// current epoch before it can finish and start the next), so the block it
+// overwrites next was read already.  A peer that never arrives turns into a
+// status-2 result after timeout_ns instead of a hang.
+__global__ void __launch_bounds__(256) p2p_finalize_kernel(const __grid_constant__ P2PArgs a) {
+  const int nv = a.fin.n + 1, tid = threadIdx.x;
+  const int buf = (int)(a.epoch & 1);
+  const size_t data_doubles = (size_t)2 * a.world * a.cap;
+  for (int q = 0; q < a.world; ++q) {
+    double* dst = reinterpret_cast<double*>(a.mbox[q]) +
+                  ((size_t)buf * a.world + a.rank) * a.cap;
+    for (int i = tid; i < nv; i += blockDim.x) dst[i] = a.slots[i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    for (int q = 0; q < a.world; ++q) {
+      uint64_t* f = reinterpret_cast<uint64_t*>(
+                        reinterpret_cast<double*>(a.mbox[q]) + data_doubles) +
+                    buf * a.world + a.rank;
+      st_release_sys(f, a.epoch);
+    }
+  }
+  __shared__ int timed_out;
+  if (tid == 0) timed_out = 0;
+  __syncthreads();
+  const double* mine = reinterpret_cast<const double*>(a.mbox[a.rank]);
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(mine + data_doubles);
+  if (tid < a.world) {
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_sys(flags + buf * a.world + tid) < a.epoch) {
+      if ((int64_t)(global_ns() - t0) > a.timeout_ns) {
+        atomicExch(&timed_out, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+    __threadfence_system();  // order this thread's acquire before the CTA's reads
+  }
+  __syncthreads();
+  if (timed_out) {
+    if (tid == 0) {
+      DevResult* res = static_cast<DevResult*>(a.fin.result);
+      res->status = COADAPT_E_INTERNAL;
+      res->sample_count = a.fin.n;
+      res->phi_available = 0;
+      res->phi = __longlong_as_double(0x7ff8000000000000ll);
+      res->state = *static_cast<DevState*>(a.fin.state);
+    }
+    return;
+  }
+  for (int i = tid; i < nv; i += blockDim.x) {
+    double v = 0.0;
+    for (int q = 0; q < a.world; ++q)
+      v += mine[((size_t)buf * a.world + q) * a.cap + i];
+    a.slots[i] = v;
+  }
+  __syncthreads();
+  if (tid == 0) finalize_body(a.fin);
 }
 
 // ---------------------------------------------------------------- K0
@@ -1446,6 +1528,11 @@ cudaError_t launch_accum(int dtype, const Range* full, int nfull, uint64_t numel
 
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
   finalize_kernel<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_finalize(const P2PArgs& a, cudaStream_t s) {
+  p2p_finalize_kernel<<<1, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -198,6 +198,21 @@ class GnsDevice:
     def allreduce(self, stream=None) -> None:
         check(lib().coadapt_gns_allreduce(self.handle, _stream(stream)))
 
+    def mailbox(self, nranks: int) -> int:
+        """This rank's NVLink slot-exchange mailbox (device address)."""
+        ptr = C.c_void_p()
+        check(lib().coadapt_gns_mailbox(self.handle, int(nranks), C.byref(ptr)))
+        return int(ptr.value)
+
+    def attach_mailboxes(self, nranks: int, rank: int, peers: Sequence[int]) -> None:
+        arr = (C.c_void_p * len(peers))(*[int(x) for x in peers])
+        check(lib().coadapt_gns_attach_mailboxes(self.handle, int(nranks), int(rank), arr))
+
+    def allreduce_finalize_p2p(self, tokens_this_step: int, stream=None) -> None:
+        """X1 + K3 in one kernel over NVLink (replaces allreduce + finalize)."""
+        check(lib().coadapt_gns_allreduce_finalize_p2p(self.handle, int(tokens_this_step),
+                                                       _stream(stream)))
+
     def finalize(self, tokens_this_step: int, stream=None) -> None:
         check(lib().coadapt_gns_finalize(self.handle, int(tokens_this_step), _stream(stream)))
 
@@ -249,6 +264,14 @@ def ipc_handle(t: torch.Tensor) -> tuple:
     buf = C.create_string_buffer(64)
     off = C.c_uint64()
     check(lib().coadapt_ipc_handle(t.data_ptr(), buf, 64, C.byref(off)))
+    return buf.raw, off.value
+
+
+def ipc_handle_ptr(ptr: int) -> tuple:
+    """ipc_handle for a raw device address (e.g. GnsDevice.mailbox)."""
+    buf = C.create_string_buffer(64)
+    off = C.c_uint64()
+    check(lib().coadapt_ipc_handle(C.c_void_p(int(ptr)), buf, 64, C.byref(off)))
     return buf.raw, off.value
 
 

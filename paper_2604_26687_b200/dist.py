@@ -44,3 +44,25 @@ def attach(gns_device, dist, world: int, rank: int) -> None:
     from .device import nccl_unique_id
     uid = share_unique_id(dist, nccl_unique_id, rank)
     gns_device.attach_nccl(world, rank, uid)
+
+
+def attach_p2p(gns_device, dist, world: int, rank: int) -> list:
+    """Give a GnsDevice NVLink mailboxes for allreduce_finalize_p2p: each
+    rank allocates its mailbox, the CUDA IPC handles are all-gathered over
+    torch.distributed, the peers' mailboxes are mapped.  Returns the base
+    pointers to pass to device.ipc_close when done."""
+    from .device import ipc_handle_ptr, ipc_open
+    mine = gns_device.mailbox(world)
+    handles = [None] * world
+    dist.all_gather_object(handles, ipc_handle_ptr(mine))
+    peers, bases = [], []
+    for q in range(world):
+        if q == rank:
+            peers.append(mine)
+        else:
+            p, b = ipc_open(handles[q], gns_device.device)
+            peers.append(p)
+            bases.append(b)
+    gns_device.attach_mailboxes(world, rank, peers)
+    dist.barrier()
+    return bases

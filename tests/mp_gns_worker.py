@@ -83,6 +83,41 @@ def main():
         dist.all_reduce(hi, op=dist.ReduceOp.MAX)
         case["phi_identical_on_all_ranks"] = bool(lo.item() == hi.item())
         ok = ok and case["phi_identical_on_all_ranks"]
+        # the same step with X1 + K3 fused into one kernel over NVLink
+        g2 = D.GnsDevice(d, M, d * M, local)
+        bases = Dist.attach_p2p(g2, dist, world, rank)
+        run_job(g2, lays, mine, M, d, 0xC0905, unit, fused)
+        g2.allreduce_finalize_p2p(d * M * 2048)
+        r2 = g2.result()
+        p2 = g2.partials()
+        case["p2p_max_rel_slots_vs_nccl"] = float(np.max(np.abs(p2 - parts) /
+                                                         np.maximum(np.abs(parts), 1e-300)))
+        case["p2p_b_simple_rel"] = abs(r2.b_simple - r.b_simple) / abs(r.b_simple)
+        t2 = torch.tensor([r2.phi], dtype=torch.float64, device="cuda")
+        lo2, hi2 = t2.clone(), t2.clone()
+        dist.all_reduce(lo2, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi2, op=dist.ReduceOp.MAX)
+        case["p2p_phi_identical_on_all_ranks"] = bool(lo2.item() == hi2.item())
+        ok = ok and case["p2p_max_rel_slots_vs_nccl"] <= 1e-14 and \
+            case["p2p_phi_identical_on_all_ranks"] and case["p2p_b_simple_rel"] <= 1e-12
+        # tail latency: NCCL all-reduce + finalize vs the fused P2P kernel
+        s = torch.cuda.current_stream()
+        for name, fn in (("nccl", lambda: (g.allreduce(), g.finalize(1))),
+                         ("p2p", lambda: g2.allreduce_finalize_p2p(1))):
+            for _ in range(5):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(50):
+                fn()
+            e1.record(s)
+            torch.cuda.synchronize()
+            case[f"tail_us_{name}"] = e0.elapsed_time(e1) / 50 * 1e3
+        dist.barrier()
+        for b in bases:
+            D.ipc_close(b)
         report["cases"].append(case)
         g.close()
     report["ok"] = bool(ok)
