@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--x1", choices=["nccl", "p2p"], default="nccl",
+                    help="slot all-reduce: NCCL, or fused with finalize over NVLink mailboxes")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-elems", type=int, default=128 << 20, help="sample elements per micro-bucket")
     return ap.parse_args()
@@ -311,6 +313,9 @@ def run_ours(args):
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         g.attach_nccl(ws, rank, obj[0])
+        if args.x1 == "p2p":
+            from paper_2604_26687_b200 import dist as Dist
+            p2p_bases = Dist.attach_p2p(g, dist, ws, rank)
 
     costs = candidate_costs(R)
     cands = G.synth_candidates(costs, [16, 32, 64, 128, 256, 512, 1024, 2048], [1, 2, 4, 8], True)
@@ -349,8 +354,11 @@ def run_ours(args):
             f0 = torch.cuda.Event(enable_timing=True)
             f1 = torch.cuda.Event(enable_timing=True)
             f0.record(stream)
-        g.allreduce(stream)
-        g.finalize(B_g * SEQ_LEN, stream)
+        if args.x1 == "p2p" and ws > 1:
+            g.allreduce_finalize_p2p(B_g * SEQ_LEN, stream)
+        else:
+            g.allreduce(stream)
+            g.finalize(B_g * SEQ_LEN, stream)
         if timed:
             f1.record(stream)
             tail_pairs.append((f0, f1))
@@ -546,6 +554,7 @@ def run_ours(args):
                            "global_batch": B_g, "bytes_per_step": job_bytes,
                            "local_bytes_per_step_rank0": local_bytes,
                            "l2": "inputs >> 126 MB L2 (each bucket streams GBs); no flush needed",
+                           "x1": args.x1 if ws > 1 else "local",
                            "pool": ("virtual ranks on one GPU share one resident set of M buckets"
                                     if R // ws > 1 else "one resident set of M buckets per rank")},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
