@@ -117,6 +117,12 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        # nvidia-smi takes ~0.1-0.5 s to start: wait for its first sample so a
+        # short timed region is still covered (and drop that warm-up sample)
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 5.0:
+            time.sleep(0.01)
+        self.skip = len(self.rows)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -132,6 +138,16 @@ class ClockSampler:
             self.proc.kill()
         if self.thread:
             self.thread.join(timeout=2)
+        rows = self.rows[getattr(self, "skip", 0):]
+        if not rows:  # region shorter than the sampling period: one query now
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits", "-i", str(self.index)],
+                                     capture_output=True, text=True, timeout=10).stdout
+                rows = [[x.strip() for x in line.split(",")] for line in out.splitlines() if line]
+            except Exception:
+                rows = []
+        self.rows = rows
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in self.rows:
