@@ -95,16 +95,73 @@ __device__ __forceinline__ void unpack<COADAPT_FP32>(const uint4& v,
   f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
 }
 
+// bf16 -> fp64 straight from the half-word (SASS F2F.F64.BF16 with a .H1
+// selector: no unpack instruction).  Exact for every bf16.
+__device__ __forceinline__ double bf16_f64(uint16_t h) {
+  double d;
+  asm("cvt.f64.bf16 %0, %1;" : "=d"(d) : "h"(h));
+  return d;
+}
+// s + x in one fp32 rounding, x a bf16 half-word read in place (SASS
+// FHFMA.BF16, x * 1.0 + s): identical to __fadd_rn(s, (float)x).
+__device__ __forceinline__ float bf16_addf(float s, uint16_t h) {
+  asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(s) : "h"(h), "h"((uint16_t)0x3F80));
+  return s;
+}
+
+// sum[e] += x_e (fp32, one rounding each) for the values of one vector: the
+// micro-batch sum of the fused pass.  bf16 via FHFMA on the packed halves,
+// the others unpacked and added pairwise with FADD2 (same rounding per lane).
+template <int DT>
+__device__ __forceinline__ void micro_add(const uint4& v, float* sum) {
+  if constexpr (DT == COADAPT_BF16) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      sum[2 * i] = bf16_addf(sum[2 * i], (uint16_t)(w[i] & 0xffffu));
+      sum[2 * i + 1] = bf16_addf(sum[2 * i + 1], (uint16_t)(w[i] >> 16));
+    }
+  } else {
+    constexpr int PV = Elem<DT>::kPerVec;
+    float f[PV];
+    unpack<DT>(v, f);
+#pragma unroll
+    for (int e = 0; e < PV; e += 2) {
+      const float2 t = __fadd2_rn(make_float2(sum[e], sum[e + 1]),
+                                  make_float2(f[e], f[e + 1]));
+      sum[e] = t.x;
+      sum[e + 1] = t.y;
+    }
+  }
+}
+
 // acc += sum of squares of one vector, every square exact in fp64.
-// bf16/fp16 -> fp32 is exact and free (a shift); fp32 -> fp64 is one F2F on
-// the XU pipe, which is what bounds these kernels at ~6.6 TB/s (1.97 GHz).
-// Cheaper variants were measured and rejected: an fp32
-// partial per vector is +5% faster but biased by ~-6e-9 relative (rounding
-// of structured bf16 squares); integer-built fp64 moves the bound to the
-// ALU/issue pipes and is slower.
+// Each value goes to fp64 with one F2F on the XU pipe (bf16 straight from
+// the half-word), which with the 1 kW power cap is what bounds these
+// kernels.  Measured alternatives (profiles/r01c_vacc_variants.txt): fp32
+// squares summed in runs of 8 (+7 % K1f, +22 % K1 sustained) is not exact;
+// building the fp64 from integer ops (half or all of the elements) moves no
+// sustained number.  Exactness was kept.
 template <int DT>
 __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
-  if constexpr (DT == COADAPT_BF16 || DT == COADAPT_FP16) {
+  if constexpr (DT == COADAPT_BF16) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    // two fp64 chains per vector halve the dependent DFMA latency
+    double a0 = bf16_f64((uint16_t)(w[0] & 0xffffu));
+    double a1 = bf16_f64((uint16_t)(w[0] >> 16));
+    a0 *= a0;
+    a1 *= a1;
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+      const double d0 = bf16_f64((uint16_t)(w[i] & 0xffffu));
+      const double d1 = bf16_f64((uint16_t)(w[i] >> 16));
+      a0 = fma(d0, d0, a0);
+      a1 = fma(d1, d1, a1);
+    }
+    acc += a0 + a1;
+    return;
+  }
+  if constexpr (DT == COADAPT_FP16) {
     float f[8];
     unpack<DT>(v, f);
     // two fp64 chains per vector halve the dependent DFMA latency
@@ -376,11 +433,8 @@ __device__ __forceinline__ void fused_piece(const FusedArgs& args, uint64_t a,
       for (int e = 0; e < PV; ++e) sum[e] = 0.0f;
 #pragma unroll
       for (int m = 0; m < M; ++m) {
-        float f[PV];
-        unpack<DT>(r[p][m], f);
         vacc<DT>(r[p][m], acc[m]);
-#pragma unroll
-        for (int e = 0; e < PV; ++e) sum[e] = __fadd_rn(sum[e], f[e]);
+        micro_add<DT>(r[p][m], sum);
       }
 #pragma unroll
       for (int e = 0; e < PV; ++e) {
@@ -397,11 +451,8 @@ __device__ __forceinline__ void fused_piece(const FusedArgs& args, uint64_t a,
     for (int m = 0; m < M; ++m) {
       const uint4 v = ld_stream(reinterpret_cast<const uint4*>(
           reinterpret_cast<uintptr_t>(args.ptr[m]) + voff + i * 16));
-      float f[PV];
-      unpack<DT>(v, f);
       vacc<DT>(v, acc[m]);
-#pragma unroll
-      for (int e = 0; e < PV; ++e) sum[e] = __fadd_rn(sum[e], f[e]);
+      micro_add<DT>(v, sum);
     }
 #pragma unroll
     for (int e = 0; e < PV; ++e) {
@@ -510,6 +561,9 @@ template <> struct TmaShape<1> { static constexpr int NW = 16, kStageBytes = 491
 template <> struct TmaShape<2> { static constexpr int NW = 8, kStageBytes = 32768; };
 template <> struct TmaShape<3> { static constexpr int NW = 8, kStageBytes = 49152; };
 template <> struct TmaShape<4> { static constexpr int NW = 16, kStageBytes = 57344; };
+// 14 consumer warps: a 3584 B tile (M = 16) is exactly 224 vectors, one per
+// thread of a 7-warp group
+template <> struct TmaShape<5> { static constexpr int NW = 14, kStageBytes = 57344; };
 
 template <int DT, int M, int V = 0>
 struct TmaCfg {
@@ -557,7 +611,6 @@ __device__ __forceinline__ void tma_consume_cols(const char* stage,
                                                  double* acc, double& gacc) {
   using C = TmaCfg<DT, M, V>;
   constexpr int VE = 16 / C::ES;
-  constexpr int UP = DT;
   const uint64_t a = cm.a, b = cm.a + cm.n;
   uint64_t A0 = (a + VE - 1) / VE * VE, A1 = b / VE * VE;
   if (A1 <= A0) A0 = A1 = b;  // no aligned interior
@@ -576,8 +629,6 @@ __device__ __forceinline__ void tma_consume_cols(const char* stage,
       asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                    : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
                    : "r"(smem_u32(stage + m * C::kTile + v * 16)));
-      float f[C::PV];
-      unpack<UP>(x, f);
       if constexpr (WEIGHTED) {
         double t = 0.0;
         vacc<DT>(x, t);
@@ -585,8 +636,7 @@ __device__ __forceinline__ void tma_consume_cols(const char* stage,
       } else {
         vacc<DT>(x, acc[m]);
       }
-#pragma unroll
-      for (int e = 0; e < C::PV; ++e) sum[e] = __fadd_rn(sum[e], f[e]);
+      micro_add<DT>(x, sum);
     }
     double g = 0.0;
 #pragma unroll
@@ -1377,10 +1427,12 @@ TmaFn tma_fn_v() {
   return f;
 }
 
-// Best shape per M, measured on B200 (bf16, 8 GB, profiles/r01_tma_shapes.txt):
-// the chunk's vectors per tile vs the group's threads and the register cap
-// decide it (e.g. M=14: shape 4 7.06 TB/s vs shape 0 5.06).
-constexpr int kBestShape[17] = {4, 4, 4, 0, 4, 4, 0, 4, 0, 4, 0, 0, 0, 0, 4, 4, 4};
+// Best shape per M, measured on B200 (bf16, 32 GB, burst,
+// profiles/r01c_tma_shapes.txt): the chunk's vectors per tile vs the group's
+// threads and the register cap decide it (e.g. M=16: shape 5's 7-warp groups
+// own exactly the 224 vectors of a 3584 B tile, 6.95 TB/s vs 6.59 for shape 4
+// whose 8-warp groups leave 32 threads idle).
+constexpr int kBestShape[17] = {4, 4, 4, 0, 4, 4, 0, 4, 0, 4, 5, 5, 0, 0, 4, 5, 5};
 
 template <int DT, int M>
 TmaFn tma_fn() {
@@ -1390,6 +1442,7 @@ TmaFn tma_fn() {
     case 2: return tma_fn_v<DT, M, 2>();
     case 3: return tma_fn_v<DT, M, 3>();
     case 4: return tma_fn_v<DT, M, 4>();
+    case 5: return tma_fn_v<DT, M, 5>();
     default: return tma_fn_v<DT, M, 0>();
   }
 }

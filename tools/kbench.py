@@ -59,6 +59,8 @@ def main():
     ap.add_argument("--fused-m", type=int, default=16)
     ap.add_argument("--fused-gb", type=float, default=16.0)
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--kernels", default="k1,probe,k1f,accum",
+                    help="comma list of k1, probe, k1f, accum")
     ap.add_argument("--sustain", type=float, default=0.0,
                     help="seconds of back-to-back launches per kernel (power-cap steady state)")
     args = ap.parse_args()
@@ -74,12 +76,16 @@ def main():
     plan = D.BucketPlan([(0, n, 1.0)], n, dt, 0)
     g = D.GnsDevice(1, args.fused_m, args.fused_m, 0)
     out = {"variant": os.environ.get("COADAPT_BF16_VARIANT", "default"), "dtype": args.dtype}
+    ks = set(args.kernels.split(","))
+    out["tma_shape"] = os.environ.get("COADAPT_TMA_SHAPE", "default")
     with torch.cuda.stream(s):
-        sec = timed(lambda: g.micro_sqnorm(plan, x, 0, 0, s), args.reps, s)
-        out["k1_gbs"] = round(n * es / sec / 1e9, 1)
+        if "k1" in ks:
+            sec = timed(lambda: g.micro_sqnorm(plan, x, 0, 0, s), args.reps, s)
+            out["k1_gbs"] = round(n * es / sec / 1e9, 1)
         sink = torch.zeros(1, dtype=torch.float64, device="cuda")
-        sec = timed(lambda: D.read_probe(x, sink, s), args.reps, s)
-        out["probe_gbs"] = round(n * es / sec / 1e9, 1)
+        if "probe" in ks:
+            sec = timed(lambda: D.read_probe(x, sink, s), args.reps, s)
+            out["probe_gbs"] = round(n * es / sec / 1e9, 1)
         del x
         torch.cuda.empty_cache()
         M = args.fused_m
@@ -88,9 +94,13 @@ def main():
         for m, b in enumerate(bufs):
             D.synth_fill(b, [(0, nb, 0, nb, nb)], 1, m, 2.0 ** -10, 1e-7)
         fplan = D.BucketPlan([(0, nb, 1.0)], nb, dt, 0)
-        sec = timed(lambda: g.fused_sqnorm(fplan, bufs, s), args.reps, s)
-        out["k1f_gbs"] = round(nb * M * es / sec / 1e9, 1)
-        out["k1f_bytes"] = nb * M * es
+        if "k1f" in ks:
+            sec = timed(lambda: g.fused_sqnorm(fplan, bufs, s), args.reps, s)
+            out["k1f_gbs"] = round(nb * M * es / sec / 1e9, 1)
+            out["k1f_bytes"] = nb * M * es
+        if "accum" not in ks:
+            print(json.dumps(out), flush=True)
+            return
         # trainer form: fp32 main_grad += grad with s_m fused, vs torch's add_
         na = nb
         main = torch.zeros(na, dtype=torch.float32, device="cuda")
