@@ -859,15 +859,27 @@ __global__ void __launch_bounds__(NT, 3)
         for (int j = 0; j < U; ++j) {
           const uint64_t v = v0 + (uint64_t)j * NT;
           if (v >= nv) continue;
-          float f[PV];
-          unpack<DT>(gr[j], f);
           float* mf = reinterpret_cast<float*>(mr[j]);
           double a0 = 0.0, a1 = 0.0, m0 = 0.0, m1 = 0.0;
+          float f[PV];
+          if constexpr (DT != COADAPT_BF16) unpack<DT>(gr[j], f);
+          const uint32_t gw[4] = {gr[j].x, gr[j].y, gr[j].z, gr[j].w};
 #pragma unroll
           for (int e = 0; e < PV; ++e) {
-            const float nvf = first ? f[e] : __fadd_rn(mf[e], f[e]);
+            float nvf;
+            double gd;
+            if constexpr (DT == COADAPT_BF16) {
+              // bf16 halves read in place: FHFMA.BF16 for the fp32 add (one
+              // rounding, == __fadd_rn), F2F.F64.BF16 for the square
+              const uint16_t h = (e & 1) ? (uint16_t)(gw[e >> 1] >> 16)
+                                         : (uint16_t)(gw[e >> 1] & 0xffffu);
+              nvf = first ? __uint_as_float((uint32_t)h << 16) : bf16_addf(mf[e], h);
+              gd = bf16_f64(h);
+            } else {
+              nvf = first ? f[e] : __fadd_rn(mf[e], f[e]);
+              gd = f[e];
+            }
             mf[e] = nvf;
-            const double gd = f[e];
             if (e & 1) a1 = fma(gd, gd, a1); else a0 = fma(gd, gd, a0);
             if (mean) {
               const double nd = nvf;

@@ -568,3 +568,45 @@ def test_randomized_layouts_k1_k1f_host(D, L, seed):
     g5.mean_sqnorm(sl, bufs[0])
     ref = O.sqnorm(hb[0], dtype, segs_sl)
     assert _rel(g5.partials()[-1], ref) <= RTOL_NORM
+
+
+# ---------------------------------------------------------------- degenerate inputs
+
+@pytest.mark.parametrize("dtype", [0, 2])
+@pytest.mark.parametrize("kind", ["no_segments", "all_weight_zero", "zero_numel"])
+def test_empty_buckets_contribute_zero(D, L, dtype, kind):
+    """A rank whose bucket holds no counted element (no segments, only TP
+    duplicates, or nothing at all) contributes exact zeros on every path and
+    the step still finalizes (s_m is a sum over local
+    parameters, empty sums are 0)."""
+    tdt = getattr(torch, TDT[dtype])
+    numel = 0 if kind == "zero_numel" else 10_001
+    segs = {"no_segments": [], "all_weight_zero": [(0, numel, 0.0)], "zero_numel": []}[kind]
+    plan = D.BucketPlan(segs, numel, dtype, 0)
+    assert plan.active_elements == 0
+    M = 4
+    bufs = [torch.ones(max(numel, 1), dtype=tdt, device="cuda")[:numel] for _ in range(M)]
+    g = D.GnsDevice(1, M, M, 0)
+    g.begin_step()
+    g.fused_sqnorm(plan, bufs)
+    assert np.all(g.partials() == 0.0)
+    g.begin_step()
+    for m in range(M):
+        g.micro_sqnorm(plan, bufs[m], 0, m)
+    g.mean_sqnorm(plan, bufs[0])
+    assert np.all(g.partials() == 0.0)
+    main = torch.full((numel,), 3.0, dtype=torch.float32, device="cuda")
+    g.begin_step()
+    g.accumulate(plan, main, bufs[0], 0, 0, first=False)
+    assert np.all(g.partials() == 0.0)
+    # accumulation itself still happens on every element (gaps included)
+    assert bool(torch.all(main == 4.0))
+    host = [b.cpu().pin_memory() for b in bufs]
+    g.begin_step()
+    g.fused_sqnorm_host(plan, host)
+    assert np.all(g.partials() == 0.0)
+    # all-zero norms: signal 0 -> phi unavailable, never an error
+    g.finalize(M * 2048)
+    r = g.result()
+    assert r.stats.signal == 0.0 and r.stats.noise == 0.0
+    assert r.status == 0 and r.phi_available == 0
