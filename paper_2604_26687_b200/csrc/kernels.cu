@@ -102,6 +102,12 @@ __device__ __forceinline__ double bf16_f64(uint16_t h) {
   asm("cvt.f64.bf16 %0, %1;" : "=d"(d) : "h"(h));
   return d;
 }
+// fp16 -> fp64 straight from the half-word (F2F.F64.F16), exact.
+__device__ __forceinline__ double f16_f64(uint16_t h) {
+  double d;
+  asm("cvt.f64.f16 %0, %1;" : "=d"(d) : "h"(h));
+  return d;
+}
 // s + x in one fp32 rounding, x a bf16 half-word read in place (SASS
 // FHFMA.BF16, x * 1.0 + s): identical to __fadd_rn(s, (float)x).
 __device__ __forceinline__ float bf16_addf(float s, uint16_t h) {
@@ -162,13 +168,15 @@ __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
     return;
   }
   if constexpr (DT == COADAPT_FP16) {
-    float f[8];
-    unpack<DT>(v, f);
-    // two fp64 chains per vector halve the dependent DFMA latency
-    double a0 = (double)f[0] * (double)f[0], a1 = (double)f[1] * (double)f[1];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    double a0 = f16_f64((uint16_t)(w[0] & 0xffffu));
+    double a1 = f16_f64((uint16_t)(w[0] >> 16));
+    a0 *= a0;
+    a1 *= a1;
 #pragma unroll
-    for (int i = 2; i < 8; i += 2) {
-      const double d0 = f[i], d1 = f[i + 1];
+    for (int i = 1; i < 4; ++i) {
+      const double d0 = f16_f64((uint16_t)(w[i] & 0xffffu));
+      const double d1 = f16_f64((uint16_t)(w[i] >> 16));
       a0 = fma(d0, d0, a0);
       a1 = fma(d1, d1, a1);
     }
