@@ -90,6 +90,10 @@ class GnsDevicePlan {
   void reduce_scatter_mean(const BucketLayout& layout,
                            std::span<const void* const> replicas, int dp_rank,
                            void* out_slice, double scale, void* stream);
+  // All-reduce form: the synchronised slice is written back into every
+  // replica in place (DDP gradient sync + gbar^2 in one pass).
+  void allreduce_mean(const BucketLayout& layout, std::span<void* const> replicas,
+                      int dp_rank, double scale, void* stream);
   void barrier(void* stream);
   void attach_nccl(int nranks, int rank, std::span<const unsigned char> id);
   void allreduce(void* stream);

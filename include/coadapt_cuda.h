@@ -247,6 +247,19 @@ int coadapt_gns_reduce_scatter_sqnorm(coadapt_gns* g, const coadapt_plan* plan,
                                       const void* const* replicas, int d,
                                       int dp_rank, void* out_slice,
                                       double scale, void* stream);
+/* All-reduce form of the same pass (DDP without a distributed optimizer):
+ * the synchronised slice is written back into [lo, hi) of EVERY replica
+ * (in place, over NVLink for the peers') instead of into an out buffer, so
+ * after the closing coadapt_gns_barrier every replica holds the whole
+ * synchronised gradient RNE_dtype(scale * fp32(sum_q replicas[q][i])) and
+ * gbar^2 has its norm: the reduce-scatter, the all-gather and the norm of
+ * Alg. 1's gradient sync in one kernel.  Only this rank
+ * touches [lo, hi) of any replica, so the in-place update cannot race.
+ * Replaces: finalize_step(acc, span mean_gradient) gns.hpp:47-48 fed by a
+ * separate all-reduce. */
+int coadapt_gns_allreduce_sqnorm(coadapt_gns* g, const coadapt_plan* plan,
+                                 void* const* replicas, int d, int dp_rank,
+                                 double scale, void* stream);
 
 /* NCCL over NVLink: sum the N+1 slots over all ranks (Alg. 1 AllReduce,
  * PAPER.md:443; the reference models it as summation). */

@@ -185,6 +185,7 @@ SIGNATURES = {
     "coadapt_ipc_close": (I, [P]),
     "coadapt_gns_barrier": (I, [P, P]),
     "coadapt_gns_reduce_scatter_sqnorm": (I, [P, P, P, I, I, P, D, P]),
+    "coadapt_gns_allreduce_sqnorm": (I, [P, P, P, I, I, D, P]),
     "coadapt_nccl_unique_id": (I, [P, SZ]),
     "coadapt_gns_attach_nccl": (I, [P, I, I, P, SZ]),
     "coadapt_gns_allreduce": (I, [P, P]),

@@ -964,10 +964,9 @@ int coadapt_gns_barrier(coadapt_gns* g, void* stream) {
   return COADAPT_OK;
 }
 
-int coadapt_gns_reduce_scatter_sqnorm(coadapt_gns* g, const coadapt_plan* p,
-                                      const void* const* replicas, int d,
-                                      int dp_rank, void* out_slice,
-                                      double scale, void* stream) {
+static int rs_common(coadapt_gns* g, const coadapt_plan* p,
+                     const void* const* replicas, int d, int dp_rank,
+                     void* out_slice, bool inplace, double scale, void* stream) {
   if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
   if (p->device != g->device)
     return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
@@ -977,7 +976,7 @@ int coadapt_gns_reduce_scatter_sqnorm(coadapt_gns* g, const coadapt_plan* p,
     return fail(COADAPT_E_VALIDATION, "fp64 buckets are not supported here");
   if (d < 1 || d > coadapt::dev::kMaxReplicas || dp_rank < 0 || dp_rank >= d)
     return fail(COADAPT_E_VALIDATION, "need 1 <= d <= 8 and 0 <= dp_rank < d");
-  if (!replicas || (p->bucket_numel && !out_slice))
+  if (!replicas || (p->bucket_numel && !inplace && !out_slice))
     return fail(COADAPT_E_VALIDATION, "replicas/out_slice is NULL");
   if (!(scale == scale) || std::isinf(scale))
     return fail(COADAPT_E_VALIDATION, "scale must be finite");
@@ -1001,7 +1000,8 @@ int coadapt_gns_reduce_scatter_sqnorm(coadapt_gns* g, const coadapt_plan* p,
   const uint64_t lo = cut(dp_rank), hi = cut(dp_rank + 1);
   a.d = d;
   a.scale = (float)scale;
-  a.out = out_slice;
+  a.out = inplace ? nullptr : out_slice;
+  a.inplace = inplace ? 1 : 0;
   a.gslot = g->N;
   GUARD(g->device);
   coadapt_plan* pm = const_cast<coadapt_plan*>(p);
@@ -1016,6 +1016,20 @@ int coadapt_gns_reduce_scatter_sqnorm(coadapt_gns* g, const coadapt_plan* p,
                              static_cast<cudaStream_t>(stream)));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return COADAPT_OK;
+}
+
+int coadapt_gns_reduce_scatter_sqnorm(coadapt_gns* g, const coadapt_plan* p,
+                                      const void* const* replicas, int d,
+                                      int dp_rank, void* out_slice,
+                                      double scale, void* stream) {
+  return rs_common(g, p, replicas, d, dp_rank, out_slice, false, scale, stream);
+}
+
+int coadapt_gns_allreduce_sqnorm(coadapt_gns* g, const coadapt_plan* p,
+                                 void* const* replicas, int d, int dp_rank,
+                                 double scale, void* stream) {
+  return rs_common(g, p, const_cast<const void* const*>(replicas), d, dp_rank,
+                   nullptr, true, scale, stream);
 }
 
 int coadapt_nccl_unique_id(void* out, size_t len) {

@@ -166,6 +166,13 @@ void GnsDevicePlan::reduce_scatter_mean(const BucketLayout& layout,
                                           out_slice, scale, stream));
 }
 
+void GnsDevicePlan::allreduce_mean(const BucketLayout& layout,
+                                   std::span<void* const> replicas, int dp_rank,
+                                   double scale, void* stream) {
+  check(coadapt_gns_allreduce_sqnorm(g_, layout.handle(), replicas.data(),
+                                     (int)replicas.size(), dp_rank, scale, stream));
+}
+
 void GnsDevicePlan::barrier(void* stream) {
   check(coadapt_gns_barrier(g_, stream));
 }

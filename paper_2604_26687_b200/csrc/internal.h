@@ -91,6 +91,7 @@ struct RSArgs {
   float scale;
   void* out;                      // this rank's slice, element lo at out[0]
   int32_t gslot;
+  int32_t inplace;                // 1: write the slice back into every replica
 };
 int occupancy_rs(int dtype);
 cudaError_t launch_rs(int dtype, const Range* full, int nfull, uint64_t lo,

@@ -941,7 +941,12 @@ __global__ void __launch_bounds__(NT, 3)
 //   out[i - lo] = RNE_dtype( scale * fp32( sum_{q = 0..d-1} rep_q[i] ) )
 // (replicas summed in fixed order) and gbar^2 += w * out^2 in fp64 — the
 // synchronised mean gradient is produced and its norm taken in ONE pass, the
-// loads coming straight from the peers' HBM over NVLink.
+// loads coming straight from the peers' HBM over NVLink.  All-reduce form
+// (inplace): the result is stored back into slice [lo, hi) of EVERY replica
+// instead of `out` — the reduce-scatter and the all-gather of a DDP gradient
+// all-reduce in the same pass (each element read once per replica and
+// written once per replica, (d-1)/d of both over NVLink: the ring optimum),
+// safe because only this rank ever touches [lo, hi) of any replica.
 
 __device__ __forceinline__ uint4 ld_peer(const uint4* p) {  // no .nc on peer memory
   uint4 r;
@@ -1021,7 +1026,12 @@ __global__ void __launch_bounds__(NT, 2)
         for (int q = 0; q < a.d; ++q)
           s = __fadd_rn(s, elem_f32<DT>(reinterpret_cast<uintptr_t>(a.rep[q]) + i * ES));
         const float o = round_dt<DT>(__fmul_rn(s, a.scale));
-        store_dt<DT>(out, i - lo, o);
+        if (a.inplace) {
+          for (int q = 0; q < a.d; ++q)
+            store_dt<DT>(static_cast<char*>(const_cast<void*>(a.rep[q])), i, o);
+        } else {
+          store_dt<DT>(out, i - lo, o);
+        }
         const double od = o;
         g = fma(w * od, od, g);
       };
@@ -1069,7 +1079,15 @@ __global__ void __launch_bounds__(NT, 2)
           }
           uint4 ov;
           pack<DT>(o, ov);
-          st_stream(reinterpret_cast<uint4*>(out + (A0 - lo) * ES) + v, ov);
+          if (a.inplace) {
+            // all-reduce form: this rank owns [lo, hi) of every replica, so
+            // the position it just read is written back nowhere else
+            for (int q = 0; q < a.d; ++q)
+              st_stream(reinterpret_cast<uint4*>(static_cast<char*>(const_cast<void*>(a.rep[q])) +
+                                                 A0 * ES) + v, ov);
+          } else {
+            st_stream(reinterpret_cast<uint4*>(out + (A0 - lo) * ES) + v, ov);
+          }
           g = fma(w, gl, g);
         }
       }

@@ -188,6 +188,15 @@ class GnsDevice:
         check(lib().coadapt_gns_reduce_scatter_sqnorm(self.handle, plan.handle, ptrs, k, int(dp_rank),
                                                       _ptr(out_slice), float(scale), _stream(stream)))
 
+    def allreduce_sqnorm(self, plan: BucketPlan, replicas: Sequence, dp_rank: int, scale: float,
+                         stream=None) -> None:
+        """All-reduce form: the synchronised slice is written back into every
+        replica (in place, peers' over NVLink) and its gbar^2 accumulated."""
+        k = len(replicas)
+        ptrs = (C.c_void_p * max(1, k))(*[_ptr(r) for r in replicas])
+        check(lib().coadapt_gns_allreduce_sqnorm(self.handle, plan.handle, ptrs, k, int(dp_rank),
+                                                 float(scale), _stream(stream)))
+
     def mean_sqnorm(self, plan: BucketPlan, mean_grad, stream=None) -> None:
         check(lib().coadapt_gns_mean_sqnorm(self.handle, plan.handle, _ptr(mean_grad), _stream(stream)))
 

@@ -3,12 +3,15 @@
 
 Each rank holds one DP replica's gradient bucket; IPC handles are exchanged
 with torch.distributed; every rank reduces its slice straight from the peers'
-HBM.  Checks (rank 0 prints one JSON line):
+HBM.  The all-reduce form (coadapt_gns_allreduce_sqnorm) writes the slice
+back into every replica in place.  Checks (rank 0 prints one JSON line):
   * the slice is bit-identical to torch: sum of the all-gathered replicas in
     replica order in fp32, times scale, rounded to the bucket dtype;
   * the all-reduced gbar^2 equals the fp64 norm of the whole synchronised
     gradient (weights applied) to 1e-12;
-  * timing against NCCL reduce_scatter_tensor + the K2 slice norm.
+  * timing against NCCL reduce_scatter_tensor + the K2 slice norm;
+  * all-reduce form: every replica bit-identical to the same reference over
+    the WHOLE bucket, gbar^2 as above, timing against NCCL all_reduce + K2.
 """
 import json
 import os
@@ -121,6 +124,98 @@ def check_case(rank, world, local, numel, dtype, bench_mb=0):
     return res
 
 
+def _open_all(x, rank, world, local):
+    hs = [None] * world
+    dist.all_gather_object(hs, D.ipc_handle(x))
+    ptrs, bases = [], []
+    for q in range(world):
+        if q == rank:
+            ptrs.append(x.data_ptr())
+        else:
+            p, b = D.ipc_open(hs[q], local)
+            ptrs.append(p)
+            bases.append(b)
+    return ptrs, bases
+
+
+def check_allreduce(rank, world, local, numel, dtype, bench_mb=0):
+    torch.manual_seed(4321 + rank)
+    tdt = TDT[dtype]
+    n = numel
+    segs = [(0, n // 3, 1.0), (n // 3, 1000, 0.0), (n // 3 + 1000, n - n // 3 - 1000, 1.0)]
+    rep = (torch.randn(n, device="cuda") * (1 + rank)).to(tdt)
+    allr = [torch.empty_like(rep) for _ in range(world)]
+    dist.all_gather(allr, rep)
+    acc = allr[0].float().clone()
+    for q in range(1, world):
+        acc.add_(allr[q].float())
+    scale = 1.0 / world
+    ref = (acc * scale).to(tdt)
+    plan = D.BucketPlan(segs, n, dtype, local)
+    g = D.GnsDevice(world, 1, world, local)
+    Dist.attach(g, dist, world, rank)
+    ptrs, bases = _open_all(rep, rank, world, local)
+    g.begin_step()
+    g.barrier()
+    g.allreduce_sqnorm(plan, ptrs, rank, scale)
+    g.barrier()
+    g.allreduce()
+    parts = g.partials()
+    torch.cuda.synchronize()
+    ok = bool(torch.equal(rep, ref))
+    w = torch.ones(n, dtype=torch.float64, device="cuda")
+    w[n // 3:n // 3 + 1000] = 0
+    g2_ref = float((w * ref.double() ** 2).sum())
+    rel = abs(parts[-1] - g2_ref) / g2_ref
+    res = {"form": "allreduce", "dtype": "bf16" if dtype == L.BF16 else "fp32", "numel": n,
+           "slice_bit_exact": ok, "gbar2_rel": rel}
+    if bench_mb:
+        big = (bench_mb << 20) // rep.element_size()
+        big -= big % (64 * world)
+        x = (torch.randn(big, device="cuda") * (1 + rank)).to(tdt)
+        bplan = D.BucketPlan([(0, big, 1.0)], big, dtype, local)
+        bp, bb = _open_all(x, rank, world, local)
+        blo, bhi = D.dp_slice(big, world, rank)
+        splan = D.BucketPlan([(0, bhi - blo, 1.0)], bhi - blo, dtype, local)
+
+        def fused():
+            g.begin_step()
+            g.barrier()
+            g.allreduce_sqnorm(bplan, bp, rank, scale)
+            g.barrier()
+
+        def nccl_then_norm():
+            # DDP's unfused form: NCCL all-reduce (sum), then the K2 norm of
+            # this rank's slice (a second read; the mean scale folded in)
+            g.begin_step()
+            dist.all_reduce(x, op=dist.ReduceOp.SUM)
+            g.mean_sqnorm(splan, x[blo:bhi])
+
+        def timed(fn, reps=10):
+            fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / reps], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+
+        res.update({"bench_bytes_per_rank": big * rep.element_size(),
+                    "fused_allreduce_ms": timed(fused),
+                    "nccl_allreduce_ms": timed(lambda: dist.all_reduce(x, op=dist.ReduceOp.SUM)),
+                    "nccl_allreduce_plus_k2_ms": timed(nccl_then_norm)})
+        bases += bb
+    for b in bases:
+        D.ipc_close(b)
+    g.close()
+    return res
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -128,7 +223,11 @@ def main():
     dist.init_process_group("nccl")
     cases = [check_case(rank, world, local, 1_000_003 - 3, L.BF16),
              check_case(rank, world, local, 777_216, L.FP32),
-             check_case(rank, world, local, 4_000_000, L.BF16, bench_mb=int(os.environ.get("RS_BENCH_MB", "0")))]
+             check_case(rank, world, local, 4_000_000, L.BF16, bench_mb=int(os.environ.get("RS_BENCH_MB", "0"))),
+             check_allreduce(rank, world, local, 1_000_003 - 3, L.BF16),
+             check_allreduce(rank, world, local, 777_216, L.FP32),
+             check_allreduce(rank, world, local, 4_000_000, L.BF16,
+                             bench_mb=int(os.environ.get("RS_BENCH_MB", "0")))]
     ok = all(c["slice_bit_exact"] and c["gbar2_rel"] <= 1e-12 for c in cases)
     t = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
