@@ -10,7 +10,11 @@ computes s_m = Σ w‖g_m‖² in the same pass (the norms cost no extra HBM
 read); on the last micro-batch of a d = 1 step it also reduces
 ‖ḡ‖² = ‖main_grad / M‖².  For d > 1 the caller synchronises main_grad
 across the DP group (sum) and hands it to ``finish_step``, which reads this
-rank's DP slice with the 1/(d·M)² scale folded into the plan weights.
+rank's DP slice with the 1/(d·M)² scale folded into the plan weights — or
+passes ``replicas`` (every DP rank's main_grad, CUDA-IPC peer pointers),
+and ``finish_step`` all-reduces main_grad itself over NVLink with ḡ² in the
+same pass (``coadapt_gns_allreduce_sqnorm``): afterwards main_grad holds the
+DP-averaged gradient, as after Megatron DDP's averaging all-reduce.
 
 Usage::
 
@@ -67,6 +71,7 @@ class GnsManager:
         self.plan = D.BucketPlan(segs, off, D.TORCH_TO_DTYPE[self.dtype], self.device)
         self.gns = D.GnsDevice(self.d, self.M, global_batch, self.device)
         self._mean_plan = None
+        self._ar_plan = None
         self._m = 0
         self._pending = 0
         self._hooks = []
@@ -106,14 +111,28 @@ class GnsManager:
         self._m = m + 1
 
     def finish_step(self, tokens: int, synced_main_grad: Optional[torch.Tensor] = None,
-                    stream=None) -> L.GnsResult:
+                    replicas=None, stream=None) -> L.GnsResult:
         """All-reduce the slots (if attached), finalize, read φ.  For d > 1
-        pass the DP-summed main_grad; this rank reads its slice of it."""
+        either pass the DP-summed main_grad (this rank reads its slice of
+        it) or ``replicas`` — the d ranks' main_grad buckets in DP order
+        (peer pointers; this rank's own tensor or pointer at dp_rank): the
+        DP all-reduce (mean) of main_grad and ḡ² then run as one NVLink pass,
+        bracketed by stream-ordered barriers."""
         if self._m != self.M:
             raise L.ValidationError(f"step has {self._m} of {self.M} micro-batches")
-        if self.d > 1:
+        if self.d > 1 and replicas is not None:
+            if len(replicas) != self.d:
+                raise L.ValidationError(f"need {self.d} replicas, got {len(replicas)}")
+            if self._ar_plan is None:
+                sc = 1.0 / float(self.M) ** 2  # out = mean over DP; gbar = out / M
+                self._ar_plan = D.BucketPlan([(o, n, w * sc) for o, n, w in self.segments],
+                                             self.numel, L.FP32, self.device)
+            self.gns.barrier(stream)
+            self.gns.allreduce_sqnorm(self._ar_plan, replicas, self.dp_rank, 1.0 / self.d, stream)
+            self.gns.barrier(stream)
+        elif self.d > 1:
             if synced_main_grad is None:
-                raise L.ValidationError("d > 1: pass the DP-summed main_grad")
+                raise L.ValidationError("d > 1: pass the DP-summed main_grad or the replicas")
             if self._mean_plan is None:
                 sc = 1.0 / float(self.d * self.M) ** 2
                 self._mean_plan = D.BucketPlan([(o, n, w * sc) for o, n, w in self.segments],

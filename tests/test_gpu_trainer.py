@@ -103,3 +103,34 @@ def test_manager_d2_slots_sum_to_reference():
     assert np.allclose(tot[:-1], s_ref, rtol=1e-12, atol=0)
     g2_ref = float((synced.double() ** 2).sum()) / (d * M) ** 2
     assert abs(tot[-1] - g2_ref) <= 1e-12 * g2_ref
+
+
+def test_manager_d2_nvlink_allreduce_form():
+    """d = 2 emulated on one GPU through the all-reduce form: each manager
+    all-reduces its slice of both replicas' main_grad in place (local
+    pointers stand in for the CUDA-IPC peers); afterwards both main_grads
+    equal the DP mean bit for bit and the slots sum to the job's values."""
+    from paper_2604_26687_b200.trainer import GnsManager
+    M, d = 2, 2
+    models = [_model(0), _model(0)]
+    data = [_data(M, 20 + r) for r in range(d)]
+    refs = [_reference(models[r], *data[r]) for r in range(d)]
+    mgrs = [GnsManager(models[r].parameters(), micro_count=M, global_batch=d * M * 8,
+                       dp_size=d, dp_rank=r) for r in range(d)]
+    for r in range(d):
+        mgrs[r].begin_step()
+        for x, y in zip(*data[r]):
+            torch.nn.functional.mse_loss(models[r](x).float(), y.float()).backward()
+            mgrs[r].after_backward()
+    mean_ref = (mgrs[0].main_grad + mgrs[1].main_grad) * 0.5  # fp32, replica order
+    reps = [mgrs[0].main_grad, mgrs[1].main_grad]
+    tot = np.zeros(d * M + 1)
+    for r in range(d):
+        mgrs[r].finish_step(tokens=d * M * 8 * 2048, replicas=reps)
+        tot += mgrs[r].gns.partials()
+    torch.cuda.synchronize()
+    assert torch.equal(mgrs[0].main_grad, mean_ref) and torch.equal(mgrs[1].main_grad, mean_ref)
+    s_ref = refs[0][2] + refs[1][2]
+    assert np.allclose(tot[:-1], s_ref, rtol=1e-12, atol=0)
+    g2_ref = float((mean_ref.double() ** 2).sum()) / M ** 2
+    assert abs(tot[-1] - g2_ref) <= 1e-12 * g2_ref
