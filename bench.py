@@ -427,7 +427,19 @@ def run_ours(args):
     # the all-reduce + finalize tail on the device, the host decide()
     red_ms = sum(a.elapsed_time(b) for a, b, _ in ev_pairs) / args.steps
     tail_ms = sum(a.elapsed_time(b) for a, b in tail_pairs) / max(1, len(tail_pairs))
+    red_all = [red_ms]
+    if ws > 1:  # per-GPU reduction time: the max-over-ranks step waits for the slowest
+        rt = torch.tensor([red_ms], dtype=torch.float64, device="cuda")
+        gat = [torch.zeros_like(rt) for _ in range(ws)]
+        dist.all_gather(gat, rt)
+        red_all = [float(x.item()) for x in gat]
+        ct = torch.tensor([float((clk or {}).get("sm_mhz") or 0.0)], dtype=torch.float64, device="cuda")
+        cg = [torch.zeros_like(ct) for _ in range(ws)]
+        dist.all_gather(cg, ct)
+        if clk is not None:
+            clk["sm_mhz_per_gpu"] = [float(x.item()) for x in cg]
     goodput_step = {"step_ms": round(ms, 4), "reductions_ms": round(red_ms, 4),
+                    "reductions_ms_per_gpu": [round(x, 4) for x in red_all],
                     "allreduce_finalize_ms": round(tail_ms, 4),
                     "decide_ms": round(1e3 * sum(decide_s) / max(1, len(decide_s)), 4),
                     "candidates": len(cands)}
