@@ -155,3 +155,57 @@ def test_c3_7b_bf16_d2t2p2_layout_invariance_full_size():
     # TP rank would change s by their (nonzero) contribution
     dup = sum(k for l in world for o, k, w in l.segments if w == 0.0)
     assert dup > 0
+
+
+def test_c4_32b_bf16_d1t4p2_fused_full_size():
+    """C4: Qwen2.5-32B bf16, (d,t,p) = (1,4,2), M = 16, the north-star job at
+    full size through K1f.  Size-independent properties (the oracle would need
+    131 GB per rank): (1) the 8 ranks' fused s_m and ||gbar||^2 summed over the
+    world equal the same sums under the (1,8,1) layout — the partition and the
+    TP-duplicate dedup are exact for this model — and (2) on rank 0 the fused
+    pass equals 16 separate K1 passes for every s_m."""
+    from paper_2604_26687_b200 import _lib as L
+    from paper_2604_26687_b200 import device as D
+    from paper_2604_26687_b200 import layout as Lay
+    torch.cuda.set_device(0)
+    torch.cuda.empty_cache()
+    spec = Lay.qwen25_32b()
+    M, seed = 16, 0xC4
+    unit = Lay.noise_unit_for(1024.0, 1)
+    worlds = {(1, 4, 2): Lay.world_layouts(spec, 1, 4, 2), (1, 8, 1): Lay.world_layouts(spec, 1, 8, 1)}
+    cap = max(l.numel for w in worlds.values() for l in w)
+    free, _ = torch.cuda.mem_get_info()
+    if M * cap * 2 > free - (8 << 30):
+        pytest.skip(f"needs {M * cap * 2 / 1e9:.0f} GB free, have {free / 1e9:.0f}")
+    bufs = [torch.empty(cap, dtype=torch.bfloat16, device="cuda") for _ in range(M)]
+    parts = {}
+    for key, world in worlds.items():
+        g = D.GnsDevice(1, M, M, 0)
+        g.begin_step()
+        for r, lay in enumerate(world):
+            views = [b[:lay.numel] for b in bufs]
+            for m in range(M):
+                D.synth_fill(views[m], lay.gen, seed, m, Lay.G0, unit)
+            plan = D.BucketPlan(lay.segments, lay.numel, L.BF16, 0)
+            g.fused_sqnorm(plan, views)
+            if key == (1, 4, 2) and r == 0:
+                sep = D.GnsDevice(1, M, M, 0)
+                sep.begin_step()
+                for m in range(M):
+                    sep.micro_sqnorm(plan, views[m], 0, m)
+                one = D.GnsDevice(1, M, M, 0)
+                one.begin_step()
+                one.fused_sqnorm(plan, views)
+                a, b = one.partials()[:M], sep.partials()[:M]
+                assert np.allclose(a, b, rtol=1e-12, atol=0), (a, b)
+                assert b.min() > 0
+                one.close()
+                sep.close()
+            plan.close()
+        parts[key] = g.partials()
+        g.close()
+    a, b = parts[(1, 4, 2)], parts[(1, 8, 1)]
+    assert np.allclose(a, b, rtol=1e-12, atol=0), (a, b)
+    assert a[M] > 0
+    del bufs
+    torch.cuda.empty_cache()
