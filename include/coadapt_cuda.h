@@ -261,6 +261,39 @@ int coadapt_gns_allreduce_sqnorm(coadapt_gns* g, const coadapt_plan* plan,
                                  void* const* replicas, int d, int dp_rank,
                                  double scale, void* stream);
 
+/* NVLS (NVLink SHARP) buckets: the switch-reduced form of the DP gradient
+ * all-reduce.  A multicast object binds one physical buffer per GPU; the
+ * trainer keeps its gradient bucket in the unicast view.  Setup, every rank
+ * (host barriers between the steps):
+ *   rank 0: coadapt_nvls_create + coadapt_nvls_export (64-byte handle: the
+ *           exporter's pid and POSIX fd, duplicated by importers with
+ *           pidfd_getfd; keep rank 0's object alive while others import)
+ *   others: coadapt_nvls_import(handle)
+ *   all:    coadapt_nvls_add_device;  barrier;  coadapt_nvls_bind -> unicast /
+ *           multicast pointers (buffer zeroed);  barrier
+ * coadapt_nvls_allreduce(o, dtype, numel, dp_rank, scale, stream): for this
+ * rank's slice (the coadapt_plan_create_slice cut) multimem.ld_reduce (the
+ * switch adds every GPU's copy), scale, multimem.st into every GPU's buffer:
+ * 1/d of the bucket per link direction instead of the (d-1)/d of
+ * coadapt_gns_allreduce_sqnorm.  fp32 buckets only (Megatron's main_grad):
+ * the switch's bf16 rounding is biased (validation error).  Bracket it with
+ * coadapt_gns_barrier; take gbar^2 of the slice with coadapt_gns_mean_sqnorm
+ * on the unicast view (sliced plan).  The switch's summation order is its
+ * own: bit-exact with the replica-order reference for d = 2, within the
+ * fp32 rounding of a d-term sum for d > 2.
+ * Replaces: the all-reduce feeding finalize_step(acc, span) gns.hpp:47-48. */
+typedef struct coadapt_nvls coadapt_nvls;
+int coadapt_nvls_create(int device, int nranks, uint64_t bytes, coadapt_nvls** out);
+int coadapt_nvls_export(const coadapt_nvls* o, void* handle, size_t len);
+int coadapt_nvls_import(int device, int nranks, uint64_t bytes, const void* handle,
+                        size_t len, coadapt_nvls** out);
+int coadapt_nvls_add_device(coadapt_nvls* o);
+int coadapt_nvls_bind(coadapt_nvls* o, void** unicast, void** multicast);
+uint64_t coadapt_nvls_bytes(const coadapt_nvls* o);
+int coadapt_nvls_allreduce(coadapt_nvls* o, int dtype, uint64_t numel, int dp_rank,
+                           double scale, void* stream);
+int coadapt_nvls_destroy(coadapt_nvls* o);
+
 /* NCCL over NVLink: sum the N+1 slots over all ranks (Alg. 1 AllReduce,
  * PAPER.md:443; the reference models it as summation). */
 int coadapt_nccl_unique_id(void* out, size_t len); /* len >= 128 */

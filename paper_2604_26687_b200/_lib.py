@@ -207,6 +207,14 @@ SIGNATURES = {
     "coadapt_gns_mean_sqnorm_host": (I, [P, P, P, P]),
     "coadapt_l2_flush": (I, [P, U64, P]),
     "coadapt_read_probe": (I, [P, U64, P, P]),
+    "coadapt_nvls_create": (I, [I, I, U64, P]),
+    "coadapt_nvls_export": (I, [P, P, SZ]),
+    "coadapt_nvls_import": (I, [I, I, U64, P, SZ, P]),
+    "coadapt_nvls_add_device": (I, [P]),
+    "coadapt_nvls_bind": (I, [P, P, P]),
+    "coadapt_nvls_bytes": (U64, [P]),
+    "coadapt_nvls_allreduce": (I, [P, I, U64, I, D, P]),
+    "coadapt_nvls_destroy": (I, [P]),
     # coadapt_host.h
     "coadapt_finalize_step": (I, [P, I64, I, D, I64, P]),
     "coadapt_finalize_step_vec": (I, [P, I64, I, P, U64, I64, P]),

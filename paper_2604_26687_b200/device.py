@@ -297,6 +297,68 @@ def ipc_close(ptr: int) -> None:
     check(lib().coadapt_ipc_close(C.c_void_p(ptr)))
 
 
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device buffer (torch.as_tensor)."""
+
+    def __init__(self, ptr: int, numel: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+class NvlsBucket:
+    """A gradient bucket in NVLS memory (coadapt_nvls_*): one physical buffer
+    per GPU bound to a multicast object; ``tensor`` is this GPU's view.  The
+    all-reduce is switch-reduced (multimem.ld_reduce / multimem.st).
+
+    Collective setup — every rank of the DP group calls it with the same
+    arguments and a torch.distributed group for the handle exchange."""
+
+    _TYPESTR = {torch.float32: "<f4", torch.float16: "<f2"}
+
+    def __init__(self, numel: int, dtype: torch.dtype, rank: int, nranks: int, dist_mod,
+                 device: Optional[int] = None):
+        dev = torch.cuda.current_device() if device is None else int(device)
+        self.dtype, self.numel, self.rank, self.nranks, self.device = dtype, int(numel), rank, nranks, dev
+        es = torch.empty((), dtype=dtype).element_size()
+        nbytes = (self.numel * es + 15) // 16 * 16
+        self.handle = C.c_void_p()
+        if rank == 0:
+            check(lib().coadapt_nvls_create(dev, nranks, nbytes, C.byref(self.handle)))
+            buf = C.create_string_buffer(64)
+            check(lib().coadapt_nvls_export(self.handle, buf, 64))
+            blob = [buf.raw]
+        else:
+            blob = [None]
+        dist_mod.broadcast_object_list(blob, src=0)
+        if rank != 0:
+            hb = C.create_string_buffer(bytes(blob[0]), 64)
+            check(lib().coadapt_nvls_import(dev, nranks, nbytes, hb, 64, C.byref(self.handle)))
+        check(lib().coadapt_nvls_add_device(self.handle))
+        dist_mod.barrier()
+        uc, mc = C.c_void_p(), C.c_void_p()
+        check(lib().coadapt_nvls_bind(self.handle, C.byref(uc), C.byref(mc)))
+        dist_mod.barrier()
+        self.unicast, self.multicast = int(uc.value), int(mc.value)
+        if dtype == torch.bfloat16:  # no bf16 typestr: view the bytes as int16
+            raw = torch.as_tensor(_CudaArray(self.unicast, self.numel, "<i2"), device=f"cuda:{dev}")
+            self.tensor = raw.view(torch.bfloat16)
+        else:
+            self.tensor = torch.as_tensor(_CudaArray(self.unicast, self.numel, self._TYPESTR[dtype]),
+                                          device=f"cuda:{dev}")
+
+    def allreduce(self, scale: float = 1.0, stream=None) -> None:
+        """tensor <- scale * sum over the group's tensors (this rank reduces
+        and broadcasts its slice; bracket with barriers)."""
+        check(lib().coadapt_nvls_allreduce(self.handle, TORCH_TO_DTYPE[self.dtype], self.numel,
+                                           self.rank, float(scale), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self.tensor = None
+            check(lib().coadapt_nvls_destroy(self.handle))
+            self.handle = None
+
+
 def dp_slice(numel: int, d: int, r: int) -> tuple:
     """[lo, hi) of DP slice r of d (the cut of coadapt_plan_create_slice)."""
     cut = lambda i: numel if i >= d else (numel * i // d) & ~63

@@ -204,3 +204,23 @@ def test_single_process_drives_all_gpus():
         r = gs[dev].result()
         assert abs(r.b_simple - ref.b_simple) <= 1e-12 * abs(ref.b_simple)
         assert np.allclose(gs[dev].partials(), one.partials(), rtol=1e-13, atol=0)
+
+
+@pytest.mark.gpu
+def test_nvls_switch_reduced_allreduce():
+    """f2, NVLS form: fp32 buckets in multicast-bound memory all-reduced by
+    the NVSwitch (multimem.ld_reduce / multimem.st); bit-exact on 2 GPUs,
+    within the d-term fp32 sum bound on 4; bf16 refused."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs (gpurun --gpus 2)")
+    world = 4 if n >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + os.getpid() % 90),
+           os.path.join(HERE, "mp_nvls_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    rep = json.loads(lines[-1])
+    assert rep["ok"], rep
