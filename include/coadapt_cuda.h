@@ -274,8 +274,8 @@ int coadapt_gns_allreduce_sqnorm(coadapt_gns* g, const coadapt_plan* plan,
  * coadapt_nvls_allreduce(o, dtype, numel, dp_rank, scale, stream): for this
  * rank's slice (the coadapt_plan_create_slice cut) multimem.ld_reduce (the
  * switch adds every GPU's copy), scale, multimem.st into every GPU's buffer:
- * 1/d of the bucket per link direction instead of the (d-1)/d of
- * coadapt_gns_allreduce_sqnorm.  fp32 buckets only (Megatron's main_grad):
+ * one bucket per link direction instead of the 2(d-1)/d of
+ * coadapt_gns_allreduce_sqnorm (equal at d = 2, 1.5x less at d = 4).  fp32 buckets only (Megatron's main_grad):
  * the switch's bf16 rounding is biased (validation error).  Bracket it with
  * coadapt_gns_barrier; take gbar^2 of the slice with coadapt_gns_mean_sqnorm
  * on the unicast view (sliced plan).  The switch's summation order is its

@@ -1,13 +1,16 @@
 // nvls.cu — NVLink SHARP (NVLS) buffers and the switch-reduced DP gradient
 // all-reduce (the step after KR).
 //
-// KR moves (d-1)/d of the bucket over each GPU's NVLink in each direction
+// KR moves 2(d-1)/d of the bucket over each GPU's NVLink in each direction
 // (peer loads + peer stores) and is link-bound at ~595 GB/s per direction
 // (profiles/r01c_kr_allreduce.txt).  With a multicast object the NVSwitch
 // does the reduction: each GPU issues `multimem.ld_reduce` for its 1/d slice
 // (the switch reads that slice from every GPU, adds, returns one copy) and
 // `multimem.st` of the scaled result (the switch writes it into every GPU's
-// buffer) — 1/d of the bucket per direction per GPU instead of (d-1)/d.
+// buffer).  Per GPU and link direction that is one bucket (out: its copies
+// of the other slices for their reductions + its own result; in: its
+// reduced slice + the others' results) instead of 2(d-1)/d buckets for the
+// P2P form — equal at d = 2, 1.5x less at d = 4, 1.75x less at d = 8.
 //
 // The buffers must be physical allocations bound to the multicast object,
 // so the trainer allocates its main_grad / grad bucket here
