@@ -14,7 +14,9 @@ rank's DP slice with the 1/(d·M)² scale folded into the plan weights — or
 passes ``replicas`` (every DP rank's main_grad, CUDA-IPC peer pointers),
 and ``finish_step`` all-reduces main_grad itself over NVLink with ḡ² in the
 same pass (``coadapt_gns_allreduce_sqnorm``): afterwards main_grad holds the
-DP-averaged gradient, as after Megatron DDP's averaging all-reduce.
+DP-averaged gradient, as after Megatron DDP's averaging all-reduce.  With
+``nvls_dist`` main_grad lives in NVLS memory and the NVSwitch does the sum
+(``coadapt_nvls_allreduce``; pays from 4 GPUs).
 
 Usage::
 
@@ -43,7 +45,11 @@ from . import device as D
 class GnsManager:
     def __init__(self, params: Iterable[torch.nn.Parameter], micro_count: int, global_batch: int,
                  dp_size: int = 1, dp_rank: int = 0,
-                 weights: Optional[Dict[torch.nn.Parameter, float]] = None, device: Optional[int] = None):
+                 weights: Optional[Dict[torch.nn.Parameter, float]] = None, device: Optional[int] = None,
+                 nvls_dist=None):
+        """nvls_dist (d > 1): a torch.distributed module/group handle; main_grad
+        is then allocated in NVLS memory (device.NvlsBucket, collective over
+        the DP group) and finish_step all-reduces it through the NVSwitch."""
         self.params = [p for p in params if p.requires_grad]
         if not self.params:
             raise L.ValidationError("no trainable parameters")
@@ -65,7 +71,12 @@ class GnsManager:
         self.numel = off
         self.segments = segs
         self.grad_bucket = torch.zeros(off, dtype=self.dtype, device=f"cuda:{self.device}")
-        self.main_grad = torch.zeros(off, dtype=torch.float32, device=f"cuda:{self.device}")
+        self._nvls = None
+        if nvls_dist is not None and self.d > 1:
+            self._nvls = D.NvlsBucket(off, torch.float32, self.dp_rank, self.d, nvls_dist, self.device)
+            self.main_grad = self._nvls.tensor  # zeroed by the bind
+        else:
+            self.main_grad = torch.zeros(off, dtype=torch.float32, device=f"cuda:{self.device}")
         for p, (o, n) in zip(self.params, self._slots):
             p.grad = self.grad_bucket[o:o + n].view_as(p)
         self.plan = D.BucketPlan(segs, off, D.TORCH_TO_DTYPE[self.dtype], self.device)
@@ -120,7 +131,19 @@ class GnsManager:
         bracketed by stream-ordered barriers."""
         if self._m != self.M:
             raise L.ValidationError(f"step has {self._m} of {self.M} micro-batches")
-        if self.d > 1 and replicas is not None:
+        if self.d > 1 and self._nvls is not None:
+            # NVLS: the switch sums the DP group's main_grad (mean), then this
+            # rank's slice of the synchronised main_grad gives its gbar^2 part
+            if self._mean_plan is None:
+                sc = 1.0 / float(self.M) ** 2
+                self._mean_plan = D.BucketPlan([(o, n, w * sc) for o, n, w in self.segments],
+                                               self.numel, L.FP32, self.device,
+                                               slice_index=self.dp_rank, slice_count=self.d)
+            self.gns.barrier(stream)
+            self._nvls.allreduce(1.0 / self.d, stream)
+            self.gns.barrier(stream)
+            self.gns.mean_sqnorm(self._mean_plan, self.main_grad, stream)
+        elif self.d > 1 and replicas is not None:
             if len(replicas) != self.d:
                 raise L.ValidationError(f"need {self.d} replicas, got {len(replicas)}")
             if self._ar_plan is None:

@@ -224,3 +224,22 @@ def test_nvls_switch_reduced_allreduce():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     rep = json.loads(lines[-1])
     assert rep["ok"], rep
+
+
+@pytest.mark.gpu
+def test_trainer_main_grad_in_nvls_memory():
+    """f1 + f2: GnsManager with nvls_dist — main_grad all-reduced by the
+    NVSwitch inside finish_step; main_grad, s_m, gbar^2 and phi vs torch."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs (gpurun --gpus 2)")
+    world = 4 if n >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29800 + os.getpid() % 90),
+           os.path.join(HERE, "mp_trainer_nvls_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    rep = json.loads(lines[-1])
+    assert rep["ok"], rep
