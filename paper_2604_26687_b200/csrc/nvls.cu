@@ -31,7 +31,6 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
-#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -389,11 +388,10 @@ int coadapt_nvls_allreduce(coadapt_nvls* o, int dtype, uint64_t numel, int dp_ra
   DevScope scope(o->device);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o->device);
-  constexpr int U = 4;
-  static const int per_sm = [] {  // development sweep: COADAPT_NVLS_CTAS_PER_SM
-    const char* e = getenv("COADAPT_NVLS_CTAS_PER_SM");
-    return e ? std::max(1, atoi(e)) : 4;
-  }();
+  // flat across 1-8 vectors in flight x 1-16 CTAs per SM on 4 GPUs (4.66-4.80
+  // ms for 2 GB, profiles/r01c_nvls_allreduce.txt): the switch path, not the
+  // SMs, sets the rate
+  constexpr int U = 4, per_sm = 4;
   const uint64_t want = (v1 - v0 + 256 * U - 1) / (256 * U);
   const int grid = (int)std::min<uint64_t>((uint64_t)sms * per_sm, std::max<uint64_t>(1, want));
   char* mc = reinterpret_cast<char*>(o->mc_va);
