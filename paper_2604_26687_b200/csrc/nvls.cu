@@ -167,10 +167,10 @@ CUmulticastObjectProp mc_prop(int nranks, uint64_t bytes) {
 }
 
 int check_args(int device, int nranks, uint64_t bytes) {
-  if (!drv().ok)
-    return fail(COADAPT_E_CUDA, "driver entry points for multicast objects are unavailable");
   if (nranks < 1 || nranks > 64 || bytes == 0 || device < 0)
     return fail(COADAPT_E_VALIDATION, "need 1 <= nranks <= 64, bytes > 0, device >= 0");
+  if (!drv().ok)
+    return fail(COADAPT_E_CUDA, "driver entry points for multicast objects are unavailable");
   int mc = 0;
   DRV(drv().DeviceGetAttribute(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, device));
   if (!mc) return fail(COADAPT_E_CUDA, "device does not support multicast objects (NVLS)");

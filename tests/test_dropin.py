@@ -56,3 +56,34 @@ def test_reference_headers_link_against_our_library(tmp_path):
 def test_span_overload_on_device(exe_ours):
     r = _run(exe_ours, "--gpu")
     assert r.returncode == 0 and r.stdout.strip().startswith("OK"), r.stdout + r.stderr
+
+
+def _build_face(out):
+    cmd = [CXX, "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(HERE, "cpp", "device_face_main.cpp"), "-L", LIBDIR, "-lcoadapt_b200",
+           f"-Wl,-rpath,{LIBDIR}", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
+@pytest.fixture(scope="module")
+def exe_face(tmp_path_factory):
+    out = str(tmp_path_factory.mktemp("face") / "device_face")
+    _build_face(out)
+    return out
+
+
+def test_device_face_links_and_fails_cleanly_without_gpu(exe_face):
+    """device.hpp / the non-reference C-ABI entry points resolve in the
+    library; without a GPU the plan throws (never aborts)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by the gpu variant")
+    r = _run(exe_face)
+    assert r.returncode == 0 and r.stdout.strip().startswith("OK"), r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_device_face_on_gpu(exe_face):
+    r = _run(exe_face, "--gpu")
+    assert r.returncode == 0 and r.stdout.strip().startswith("OK"), r.stdout + r.stderr
