@@ -412,7 +412,7 @@ bool use_tma_path() {
 
 int launch_fused_tma_all(coadapt_gns* g, coadapt_plan* p, const FusedArgs& fa,
                          int M, cudaStream_t s) {
-  const int P = coadapt::dev::tma_chunk_elems(p->dtype, M);
+  const int P = coadapt::dev::tma_chunk_elems(p->dtype, M, fa.gslot >= 0);
   if (P <= 0) return fail(COADAPT_E_INTERNAL, "no TMA kernel for this dtype/M");
   const coadapt_plan::Chunks* ch = nullptr;
   if (int rc = plan_chunks(p, P, &ch)) return rc;
@@ -692,6 +692,29 @@ int coadapt_gns_micro_sqnorm_batched(coadapt_gns* g, const coadapt_plan* p,
     return fail(COADAPT_E_VALIDATION, "bad batch arguments");
   GUARD(g->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // 2..16 16-byte-aligned buckets into consecutive slots (one rank's micro-
+  // batches): the TMA ring of the fused pass without its mean term, which
+  // streams at a higher rate than the LDG form (profiles/r01c_k1_tma.txt)
+  if (use_tma_path() && count >= 2 && count <= coadapt::dev::kMaxFusedM) {
+    bool ok = true;
+    for (int j = 0; j < count && ok; ++j) {
+      ok = (reinterpret_cast<uintptr_t>(buckets[j]) & 15) == 0 &&
+           dp_index[j] * g->M + micro[j] == dp_index[0] * g->M + micro[0] + j;
+    }
+    if (ok) {
+      FusedArgs fa;
+      std::memset(&fa, 0, sizeof(fa));
+      for (int j = 0; j < count; ++j) {
+        if (int rc = check_slot(g, dp_index[j], micro[j])) return rc;
+        if (int rc = check_bucket(p, buckets[j], "bucket")) return rc;
+        fa.ptr[j] = buckets[j];
+      }
+      fa.slot0 = dp_index[0] * g->M + micro[0];
+      fa.gslot = -1;
+      fa.gscale = 0.0;
+      return launch_fused_tma_all(g, const_cast<coadapt_plan*>(p), fa, count, s);
+    }
+  }
   for (int base = 0; base < count; base += coadapt::dev::kMaxBatch) {
     BatchArgs jobs;
     std::memset(&jobs, 0, sizeof(jobs));

@@ -59,7 +59,7 @@ cudaError_t launch_fused(int dtype, int M, const Range* ranges, int nranges,
 // TMA form of the fused pass (one CTA per SM).  Chunks are numbered range by
 // range: range k owns chunks [prefix[k], prefix[k+1]) covering its
 // intersections with the absolute windows [j*P, (j+1)*P).
-int tma_chunk_elems(int dtype, int M);  // P
+int tma_chunk_elems(int dtype, int M, bool mean = true);  // P
 cudaError_t launch_fused_tma(int dtype, int M, const Range* ranges, int nranges,
                              const uint64_t* prefix, uint64_t c_begin,
                              uint64_t c_end, const FusedArgs& args, Sink sink,

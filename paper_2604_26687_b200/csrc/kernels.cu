@@ -612,7 +612,7 @@ __device__ __forceinline__ float elem_at(const FusedArgs& args, int m,
 // and the M values of each element are summed in micro-batch order in fp32
 // (Megatron main_grad order), the sum squared in fp64.  The <16-byte edges
 // of a range come from global memory.
-template <int DT, int M, int V, int GT, bool WEIGHTED>
+template <int DT, int M, int V, int GT, bool WEIGHTED, bool MEAN>
 __device__ __forceinline__ void tma_consume_cols(const char* stage,
                                                  const FusedArgs& args,
                                                  const ChunkMeta& cm, int gt,
@@ -644,15 +644,17 @@ __device__ __forceinline__ void tma_consume_cols(const char* stage,
       } else {
         vacc<DT>(x, acc[m]);
       }
-      micro_add<DT>(x, sum);
+      if constexpr (MEAN) micro_add<DT>(x, sum);
     }
-    double g = 0.0;
+    if constexpr (MEAN) {
+      double g = 0.0;
 #pragma unroll
-    for (int e = 0; e < C::PV; ++e) {
-      const double sd = sum[e];
-      g = fma(sd, sd, g);
+      for (int e = 0; e < C::PV; ++e) {
+        const double sd = sum[e];
+        g = fma(sd, sd, g);
+      }
+      gacc = WEIGHTED ? fma(w, g, gacc) : gacc + g;
     }
-    gacc = WEIGHTED ? fma(w, g, gacc) : gacc + g;
   }
   for (int q = gt; q < nhead + ntail; q += GT) {
     const uint64_t i = q < nhead ? a + q : A1 + (q - nhead);
@@ -664,12 +666,14 @@ __device__ __forceinline__ void tma_consume_cols(const char* stage,
       acc[m] = fma(WEIGHTED ? w * xd : xd, xd, acc[m]);
       sum = __fadd_rn(sum, x);
     }
-    const double sd = sum;
-    gacc = fma(WEIGHTED ? w * sd : sd, sd, gacc);
+    if constexpr (MEAN) {
+      const double sd = sum;
+      gacc = fma(WEIGHTED ? w * sd : sd, sd, gacc);
+    }
   }
 }
 
-template <int DT, int M, int V>
+template <int DT, int M, int V, bool MEAN>
 __global__ void __launch_bounds__(TmaCfg<DT, M, V>::NT, 1)
     fused_tma_kernel(const Range* __restrict__ R, int nr,
                      const uint64_t* __restrict__ prefix, uint64_t c_begin,
@@ -695,6 +699,7 @@ __global__ void __launch_bounds__(TmaCfg<DT, M, V>::NT, 1)
   }
   __syncthreads();
   const uint64_t G = gridDim.x;
+  // !MEAN: batched K1 over M buckets sharing the layout (no mean term)
   double acc[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) acc[m] = 0.0;
@@ -737,11 +742,11 @@ __global__ void __launch_bounds__(TmaCfg<DT, M, V>::NT, 1)
       mbar_wait(&full[st], (uint32_t)((i / C::kStages) & 1));
       const ChunkMeta cm = meta[st];
       if (cm.w == 1.0)
-        tma_consume_cols<DT, M, V, GW * 32, false>(smem + st * C::kStage, args, cm,
-                                                gt, acc, gtotal);
+        tma_consume_cols<DT, M, V, GW * 32, false, MEAN>(smem + st * C::kStage, args, cm,
+                                                      gt, acc, gtotal);
       else
-        tma_consume_cols<DT, M, V, GW * 32, true>(smem + st * C::kStage, args, cm,
-                                               gt, acc, gtotal);
+        tma_consume_cols<DT, M, V, GW * 32, true, MEAN>(smem + st * C::kStage, args, cm,
+                                                     gt, acc, gtotal);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
@@ -751,7 +756,7 @@ __global__ void __launch_bounds__(TmaCfg<DT, M, V>::NT, 1)
     const double v = block_sum<C::NT>(acc[m], red);
     if (threadIdx.x == 0) sink.partials[(size_t)m * G + blockIdx.x] = v;
   }
-  {
+  if constexpr (MEAN) {
     const double v = block_sum<C::NT>(gtotal, red);
     if (threadIdx.x == 0) sink.partials[(size_t)M * G + blockIdx.x] = v;
   }
@@ -760,7 +765,7 @@ __global__ void __launch_bounds__(TmaCfg<DT, M, V>::NT, 1)
         threadIdx.x < M ? args.slot0 + (int)threadIdx.x : args.gslot;
     out_scale[threadIdx.x] = threadIdx.x < M ? 1.0 : args.gscale;
   }
-  last_cta_combine<C::NT>(sink, M + 1, out_slot, out_scale, red);
+  last_cta_combine<C::NT>(sink, MEAN ? M + 1 : M, out_slot, out_scale, red);
 }
 
 // ---------------------------------------------------------------- KA
@@ -1448,11 +1453,11 @@ struct TmaFn {
   int P = 0, smem = 0, nt = 0;
 };
 
-template <int DT, int M, int V>
+template <int DT, int M, int V, bool MEAN>
 TmaFn tma_fn_v() {
   using C = TmaCfg<DT, M, V>;
   TmaFn f;
-  f.fn = reinterpret_cast<void*>(&fused_tma_kernel<DT, M, V>);
+  f.fn = reinterpret_cast<void*>(&fused_tma_kernel<DT, M, V, MEAN>);
   f.P = C::P;
   f.smem = C::kSmem;
   f.nt = C::NT;
@@ -1473,24 +1478,26 @@ TmaFn tma_fn_v() {
 constexpr int kBestShape[17] = {4, 4, 4, 0, 4, 4, 0, 4, 0, 4, 5, 5, 0, 0, 4, 5, 5};
 
 template <int DT, int M>
-TmaFn tma_fn() {
+TmaFn tma_fn(bool mean) {
+  // batched K1 (no mean term): the best shape only
+  if (!mean) return tma_fn_v<DT, M, kBestShape[M], false>();
   static const char* e = getenv("COADAPT_TMA_SHAPE");  // development sweep
   switch (e ? atoi(e) : kBestShape[M]) {
-    case 1: return tma_fn_v<DT, M, 1>();
-    case 2: return tma_fn_v<DT, M, 2>();
-    case 3: return tma_fn_v<DT, M, 3>();
-    case 4: return tma_fn_v<DT, M, 4>();
-    case 5: return tma_fn_v<DT, M, 5>();
-    default: return tma_fn_v<DT, M, 0>();
+    case 1: return tma_fn_v<DT, M, 1, true>();
+    case 2: return tma_fn_v<DT, M, 2, true>();
+    case 3: return tma_fn_v<DT, M, 3, true>();
+    case 4: return tma_fn_v<DT, M, 4, true>();
+    case 5: return tma_fn_v<DT, M, 5, true>();
+    default: return tma_fn_v<DT, M, 0, true>();
   }
 }
 
 template <int DT>
-TmaFn tma_fn_rt(int M) {
+TmaFn tma_fn_rt(int M, bool mean) {
   switch (M) {
 #define F(m) \
   case m:    \
-    return tma_fn<DT, m>();
+    return tma_fn<DT, m>(mean);
     F(1) F(2) F(3) F(4) F(5) F(6) F(7) F(8) F(9) F(10) F(11) F(12) F(13) F(14)
         F(15) F(16)
 #undef F
@@ -1498,24 +1505,24 @@ TmaFn tma_fn_rt(int M) {
   return TmaFn{};
 }
 
-TmaFn tma_kernel(int dtype, int M) {
+TmaFn tma_kernel(int dtype, int M, bool mean) {
   switch (dtype) {
-    case COADAPT_BF16: return tma_fn_rt<COADAPT_BF16>(M);
-    case COADAPT_FP16: return tma_fn_rt<COADAPT_FP16>(M);
-    case COADAPT_FP32: return tma_fn_rt<COADAPT_FP32>(M);
+    case COADAPT_BF16: return tma_fn_rt<COADAPT_BF16>(M, mean);
+    case COADAPT_FP16: return tma_fn_rt<COADAPT_FP16>(M, mean);
+    case COADAPT_FP32: return tma_fn_rt<COADAPT_FP32>(M, mean);
   }
   return TmaFn{};
 }
 
 }  // namespace
 
-int tma_chunk_elems(int dtype, int M) { return tma_kernel(dtype, M).P; }
+int tma_chunk_elems(int dtype, int M, bool mean) { return tma_kernel(dtype, M, mean).P; }
 
 cudaError_t launch_fused_tma(int dtype, int M, const Range* ranges, int nranges,
                              const uint64_t* prefix, uint64_t c_begin,
                              uint64_t c_end, const FusedArgs& fa, Sink sink,
                              int grid, cudaStream_t s) {
-  const TmaFn f = tma_kernel(dtype, M);
+  const TmaFn f = tma_kernel(dtype, M, fa.gslot >= 0);
   if (!f.fn) return cudaErrorInvalidValue;
   void* args[] = {(void*)&ranges, (void*)&nranges, (void*)&prefix,
                   (void*)&c_begin, (void*)&c_end, (void*)&fa, (void*)&sink};

@@ -610,3 +610,33 @@ def test_empty_buckets_contribute_zero(D, L, dtype, kind):
     r = g.result()
     assert r.stats.signal == 0.0 and r.stats.noise == 0.0
     assert r.status == 0 and r.phi_available == 0
+
+
+@pytest.mark.parametrize("dtype", [0, 1, 2])
+@pytest.mark.parametrize("M", [2, 5, 8, 16])
+def test_batched_k1_tma_ring_matches_single_passes(D, L, dtype, M):
+    """micro_sqnorm_batched over one rank's aligned micro-buckets runs the TMA
+    ring without its mean term; it must equal the single-bucket K1 passes
+    (and the oracle), touch only the M slots, and fall back to the LDG batch
+    for unaligned views with the same results."""
+    numel = 300_007
+    segs = [(0, 100_000, 1.0), (100_000, 3333, 0.0), (103_333, numel - 103_333 - 7, 0.5)]
+    gen = [(0, numel, 0, numel, numel)]
+    unit = O.noise_unit_for(2 ** -10, 64.0, 1)
+    plan = D.BucketPlan(segs, numel, dtype, 0)
+    d = 2
+    for off in (0, 1):
+        bufs = [_dev_buf(D, numel, dtype, gen, 31, m, unit, offset_elems=off)[1] for m in range(M)]
+        gb = D.GnsDevice(d, M, d * M, 0)
+        gb.begin_step()
+        gb.micro_sqnorm_batched(plan, bufs, [1] * M, list(range(M)))
+        gs = D.GnsDevice(d, M, d * M, 0)
+        gs.begin_step()
+        for m in range(M):
+            gs.micro_sqnorm(plan, bufs[m], 1, m)
+        pb, ps = gb.partials(), gs.partials()
+        assert np.all(pb[:M] == 0.0) and pb[-1] == 0.0  # only dp_index 1's slots
+        assert np.allclose(pb[M:2 * M], ps[M:2 * M], rtol=1e-12, atol=0), (off, pb, ps)
+        for m in (0, M - 1):
+            ref = O.sqnorm(_host_u(bufs[m]), dtype, segs)
+            assert _rel(pb[M + m], ref) <= RTOL_NORM
