@@ -509,6 +509,29 @@ int stream_host_k1(coadapt_gns* g, const coadapt_plan* p, const void* host,
   return COADAPT_OK;
 }
 
+// K1 over 1..16 buckets sharing plan p through the fused pass's TMA ring
+// without its mean term, when every bucket is 16-byte aligned: the same exact
+// arithmetic as the LDG batch at a higher rate under the power cap (single
+// bucket 6.77 -> 7.33 TB/s burst, 5.97 -> 6.79 sustained; C2 step +13 %,
+// profiles/r01c_k1_tma.txt).  Returns false (nothing launched) when the
+// buckets do not qualify; *rc is the launch status otherwise.
+bool try_tma_k1(coadapt_gns* g, const coadapt_plan* p, const void* const* buckets,
+                int count, int slot0, cudaStream_t s, int* rc) {
+  if (!use_tma_path() || count < 1 || count > coadapt::dev::kMaxFusedM) return false;
+  for (int j = 0; j < count; ++j)
+    if (!buckets[j] || (reinterpret_cast<uintptr_t>(buckets[j]) & 15)) return false;
+  FusedArgs fa;
+  std::memset(&fa, 0, sizeof(fa));
+  for (int j = 0; j < count; ++j) {
+    if ((*rc = check_bucket(p, buckets[j], "bucket"))) return true;
+    fa.ptr[j] = buckets[j];
+  }
+  fa.slot0 = slot0;
+  fa.gslot = -1;
+  *rc = launch_fused_tma_all(g, const_cast<coadapt_plan*>(p), fa, count, s);
+  return true;
+}
+
 }  // namespace
 
 // ====================================================================== API
@@ -692,27 +715,17 @@ int coadapt_gns_micro_sqnorm_batched(coadapt_gns* g, const coadapt_plan* p,
     return fail(COADAPT_E_VALIDATION, "bad batch arguments");
   GUARD(g->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // 2..16 16-byte-aligned buckets into consecutive slots (one rank's micro-
-  // batches): the TMA ring of the fused pass without its mean term, which
-  // streams at a higher rate than the LDG form (profiles/r01c_k1_tma.txt)
-  if (use_tma_path() && count >= 2 && count <= coadapt::dev::kMaxFusedM) {
-    bool ok = true;
-    for (int j = 0; j < count && ok; ++j) {
-      ok = (reinterpret_cast<uintptr_t>(buckets[j]) & 15) == 0 &&
-           dp_index[j] * g->M + micro[j] == dp_index[0] * g->M + micro[0] + j;
+  // 1..16 16-byte-aligned buckets into consecutive slots (one rank's micro-
+  // batches): the TMA ring of the fused pass without its mean term
+  if (count >= 1 && count <= coadapt::dev::kMaxFusedM) {
+    bool contiguous = true;
+    for (int j = 0; j < count && contiguous; ++j) {
+      if (int rc = check_slot(g, dp_index[j], micro[j])) return rc;
+      contiguous = dp_index[j] * g->M + micro[j] == dp_index[0] * g->M + micro[0] + j;
     }
-    if (ok) {
-      FusedArgs fa;
-      std::memset(&fa, 0, sizeof(fa));
-      for (int j = 0; j < count; ++j) {
-        if (int rc = check_slot(g, dp_index[j], micro[j])) return rc;
-        if (int rc = check_bucket(p, buckets[j], "bucket")) return rc;
-        fa.ptr[j] = buckets[j];
-      }
-      fa.slot0 = dp_index[0] * g->M + micro[0];
-      fa.gslot = -1;
-      fa.gscale = 0.0;
-      return launch_fused_tma_all(g, const_cast<coadapt_plan*>(p), fa, count, s);
+    if (contiguous) {
+      int rc = -1;
+      if (try_tma_k1(g, p, buckets, count, dp_index[0] * g->M + micro[0], s, &rc)) return rc;
     }
   }
   for (int base = 0; base < count; base += coadapt::dev::kMaxBatch) {
@@ -779,6 +792,11 @@ int coadapt_gns_mean_sqnorm(coadapt_gns* g, const coadapt_plan* p,
     return fail(COADAPT_E_VALIDATION, "fp64: use coadapt_sqnorm_device");
   if (int rc = check_bucket(p, mean_grad, "mean_grad")) return rc;
   GUARD(g->device);
+  {
+    int rc = -1;
+    if (try_tma_k1(g, p, &mean_grad, 1, g->N, static_cast<cudaStream_t>(stream), &rc))
+      return rc;
+  }
   BatchArgs jobs;
   std::memset(&jobs, 0, sizeof(jobs));
   jobs.count = 1;
