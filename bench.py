@@ -449,7 +449,7 @@ def run_ours(args):
     byts = [x for _, _, x in ev_pairs]
     achieved = sum(byts) / sum(durs) / 1e9
     peak, peak_kind = read_peak()
-    kname = "fused_tma_kernel (K1f)" if fused else "sqnorm_kernel (K1)"
+    kname = "fused_tma_kernel (K1f)" if fused else "fused_tma_kernel<MEAN=false> (K1 on the TMA ring)"
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config),
             "kernel": kname, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, copy)",
