@@ -18,6 +18,8 @@
 // SM.  Weight-0 ranges (TP duplicates) are never loaded.  Every square is
 // exact in fp64 and summed in fp64; CTA partials are combined by the last
 // CTA in a fixed order, so results are bit-reproducible run to run.
+#include <atomic>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -1461,11 +1463,16 @@ TmaFn tma_fn_v() {
   f.P = C::P;
   f.smem = C::kSmem;
   f.nt = C::NT;
-  static bool attr = false;  // opt in to > 48 KB dynamic shared memory once
-  if (!attr) {
+  // opt in to > 48 KB dynamic shared memory once per device (the attribute
+  // is per device: one process may drive several GPUs)
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
     cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          C::kSmem);
-    attr = true;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   return f;
 }
