@@ -1,11 +1,12 @@
 // kernels.cu — sm_100a kernels of the GNS hot path.
 //
-//   K1  sqnorm_kernel  : s += sum_ranges w * ||bucket[range]||^2 for a batch
-//                        of buckets sharing one layout, and
-//                        the d > 1 mean-gradient read.
-//   K1f fused_tma_kernel: d = 1: all M micro-buckets of a rank in one pass
-//                        (TMA bulk ring), every s_m plus ||sum_m g_m||^2;
-//                        fused_kernel is its LDG form for unaligned buckets.
+//   K1  s += sum_ranges w * ||bucket[range]||^2 for 1..16 buckets sharing one
+//       layout and the d > 1 mean-gradient read
+//       (PAPER.md:444-445): fused_tma_kernel<..., MEAN=false> (TMA bulk ring)
+//       for 16-byte-aligned buckets, sqnorm_kernel (LDG) for unaligned views.
+//   K1f fused_tma_kernel<..., MEAN=true>: d = 1: all M micro-buckets of a
+//       rank in one pass, every s_m plus ||sum_m g_m||^2; fused_kernel is
+//       its LDG form for unaligned buckets.
 //   KA  accum_kernel   : trainer form, fp32 grad accumulation + s_m (+ gbar^2).
 //   K3  finalize_kernel: finalize_step + update_ema + gns (gns.hpp:42-73).
 //   K0  synth kernels  : integer-exact synthetic gradients (test/bench data).
@@ -13,9 +14,11 @@
 // Bandwidth design (B200, HBM3e): the reductions are pure streams.  The
 // active elements are cut into chunks assigned CTA c <- chunk c mod G, so
 // all CTAs sweep HBM together (7.35 TB/s read ceiling measured by
-// tools/bw_sweep.cu, vs ~6.5 TB/s for contiguous per-CTA shares); 128-bit
-// ld.global.nc.L1::no_allocate loads, U in flight per thread, 4 CTAs per
-// SM.  Weight-0 ranges (TP duplicates) are never loaded.  Every square is
+// tools/bw_sweep.cu, vs ~6.5 TB/s for contiguous per-CTA shares).  The TMA
+// ring (one producer lane, cp.async.bulk into a 4-stage shared-memory ring,
+// consumer warps on LDS) is the main path: under the 1 kW power cap it
+// streams ~14 % faster than 128-bit LDG loads with the same arithmetic.
+// Weight-0 ranges (TP duplicates) are never loaded.  Every square is
 // exact in fp64 and summed in fp64; CTA partials are combined by the last
 // CTA in a fixed order, so results are bit-reproducible run to run.
 #include <atomic>
