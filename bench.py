@@ -589,7 +589,13 @@ def run_ours(args):
                 "goodput_step": goodput_step,
                 "clocks": clk,
                 "result": {"phi": r.phi if r.phi_available else None, "b_simple": r.b_simple,
-                           "signal": r.stats.signal, "noise": r.stats.noise}}
+                           "signal": r.stats.signal, "noise": r.stats.noise,
+                           "gradient": ("replicated: the virtual ranks on a GPU reduce the same "
+                                        "resident buckets, so phi is that of a job whose ranks hold "
+                                        "identical shards (the bytes streamed are the job's); the "
+                                        "job's own phi is checked against the oracle in "
+                                        "tests/test_gpu_fullsize_oracle.py"
+                                        if R // ws > 1 else "each rank its own shard")}}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()

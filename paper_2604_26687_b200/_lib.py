@@ -145,6 +145,25 @@ class ReshardInfoC(C.Structure):
                 ("src_max_pack_numel", C.c_uint64), ("dst_max_pack_numel", C.c_uint64)]
 
 
+class GradTensorC(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("stage", C.c_int32), ("ndim", C.c_int32),
+                ("tp_axis", C.c_int32), ("reserved_", C.c_int32), ("shape", C.c_int64 * 4)]
+
+
+class GradModelC(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("layers", C.c_int32), ("tied", C.c_int32),
+                ("tensors", C.POINTER(GradTensorC)), ("n_tensors", C.c_size_t)]
+
+
+class SegmentC(C.Structure):
+    _fields_ = [("offset", C.c_uint64), ("numel", C.c_uint64), ("weight", C.c_double)]
+
+
+class GenSegmentC(C.Structure):
+    _fields_ = [("local_off", C.c_uint64), ("numel", C.c_uint64), ("global_base", C.c_uint64),
+                ("row_len", C.c_uint64), ("row_stride", C.c_uint64)]
+
+
 class ClockC(C.Structure):
     _fields_ = [("elapsed", C.c_double), ("useful", C.c_double), ("reconfig_total", C.c_double),
                 ("reconfigs", C.c_int64)]
@@ -250,6 +269,10 @@ SIGNATURES = {
     "coadapt_reshard_plan_csv": (I, [P, P, SZ, P]),
     "coadapt_reshard_latency": (I, [P, D, D, P]),
     "coadapt_reshard_execute": (I, [P, I, I, P, SZ, P, SZ, I, I, P]),
+    # coadapt_segments.h
+    "coadapt_model_preset": (I, [C.c_char_p, P]),
+    "coadapt_gns_segments": (I, [P, I, I, I, I, P, P, SZ, P, P, P]),
+    "coadapt_gns_algorithmic_bytes": (I, [P, I, I, I, I, I, I, P]),
 }
 
 _lib = None
@@ -282,7 +305,7 @@ def check(rc: int) -> None:
 def header_symbols() -> list[str]:
     """Every function declared in the C-ABI headers under include/."""
     names = []
-    for h in ("coadapt_cuda.h", "coadapt_host.h", "coadapt_reshard.h"):
+    for h in ("coadapt_cuda.h", "coadapt_host.h", "coadapt_reshard.h", "coadapt_segments.h"):
         text = open(os.path.join(INCLUDE_DIR, h)).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         names += re.findall(r"\b(coadapt_[a-z0-9_]+)\s*\(", text)

@@ -209,3 +209,52 @@ def algorithmic_bytes(spec: ModelSpec, d: int, t: int, p: int, M: int, esize: in
     # mean read: each model-parallel shard read once per box (d slices)
     mean = 0 if (fused and d == 1) else sum(l.counted for l in lay if l.coords[0] == 0) * esize
     return micro + mean
+
+
+# ---------------------------------------------------------------- native twin
+
+_STAGE = {"embed": 0, "layer": 1, "final": 2, "head": 3}
+
+
+def to_native(spec: ModelSpec):
+    """The spec as a coadapt_grad_model (coadapt_segments.h); returns the
+    struct and the ctypes objects it points into (keep both alive)."""
+    import ctypes as C
+    from . import _lib as L
+    ts = [t for t in spec.embed] + [t for t in spec.per_layer] + [t for t in spec.final]
+    if not spec.tied:
+        ts += [t for t in spec.head]
+    arr = (L.GradTensorC * max(1, len(ts)))()
+    names = []
+    for i, t in enumerate(ts):
+        nm = C.c_char_p(t.name.encode())
+        names.append(nm)
+        arr[i].name = nm.value
+        arr[i].stage = _STAGE[t.stage]
+        arr[i].ndim = len(t.shape)
+        arr[i].tp_axis = -1 if t.split_axis is None else int(t.split_axis)
+        for a, n in enumerate(t.shape):
+            arr[i].shape[a] = int(n)
+    nm = spec.name.encode()
+    m = L.GradModelC(nm, spec.layers, 1 if spec.tied else 0, arr, len(ts))
+    return m, (arr, names, nm)
+
+
+def native_rank_layout(spec: ModelSpec, d: int, t: int, p: int, rank: int) -> RankLayout:
+    """rank_layout() computed by the library's C++ generator
+    (coadapt::gns_segments through coadapt_gns_segments)."""
+    import ctypes as C
+    from . import _lib as L
+    m, keep = to_native(spec)
+    cnt, numel, coords = C.c_size_t(0), C.c_uint64(0), (C.c_int32 * 3)()
+    L.check(L.lib().coadapt_gns_segments(C.byref(m), d, t, p, rank, None, None, 0, C.byref(cnt),
+                                         C.byref(numel), coords))
+    n = cnt.value
+    segs, gens = (L.SegmentC * max(1, n))(), (L.GenSegmentC * max(1, n))()
+    L.check(L.lib().coadapt_gns_segments(C.byref(m), d, t, p, rank, segs, gens, n, C.byref(cnt),
+                                         C.byref(numel), coords))
+    del keep
+    return RankLayout(rank, (coords[0], coords[1], coords[2]), numel.value,
+                      [(s.offset, s.numel, s.weight) for s in segs[:n]],
+                      [(g.local_off, g.numel, g.global_base, g.row_len, g.row_stride) for g in gens[:n]],
+                      [])

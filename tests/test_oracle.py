@@ -8,6 +8,7 @@ tests/golden/make_spec_golden.py) and its statistical properties
 import json
 import math
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -314,3 +315,26 @@ def test_fused_matches_separate_passes():
     w = np.ones(n)
     w[50_000:50_003] = 0
     assert ss == pytest.approx(float((w * acc.astype(np.float64) ** 2).sum()), rel=1e-12)
+
+
+def test_window_crop_helpers_reproduce_whole_bucket():
+    """tests/test_gpu_fullsize_oracle.py reduces full-size buckets window by
+    window; its crop helpers must reproduce the whole-bucket generator bytes
+    and segment sums for every cut, including cuts inside a TP-split row."""
+    import numpy as np
+    from paper_2604_26687_b200 import layout as Lay
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_gpu_fullsize_oracle import crop_gen, crop_segments
+    spec = Lay.tiny_model(layers=4, h=64, ffn=128, vocab=96)
+    for d, t, p in [(1, 2, 2), (2, 2, 1), (1, 4, 1)]:
+        for lay in Lay.world_layouts(spec, d, t, p):
+            full = O.synth_fill(lay.numel, O.BF16, lay.gen, 7, 3, Lay.G0, 1e-6)
+            cuts = [(0, lay.numel), (13, 777), (1000, lay.numel - 5),
+                    (lay.numel // 3, lay.numel // 3 + 4097)]
+            for a, b in cuts:
+                w = O.synth_fill(b - a, O.BF16, crop_gen(lay.gen, a, b), 7, 3, Lay.G0, 1e-6)
+                assert np.array_equal(w, full[a:b])
+                s1 = O.sqnorm(full[a:b], O.BF16, crop_segments(lay.segments, a, b))
+                s2 = O.sqnorm(full, O.BF16, [(o + a, k, x) for o, k, x in
+                                              crop_segments(lay.segments, a, b)])
+                assert s1 == s2
