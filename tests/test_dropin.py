@@ -87,3 +87,74 @@ def test_device_face_links_and_fails_cleanly_without_gpu(exe_face):
 def test_device_face_on_gpu(exe_face):
     r = _run(exe_face, "--gpu")
     assert r.returncode == 0 and r.stdout.strip().startswith("OK"), r.stdout + r.stderr
+
+
+def _build_face_run(out):
+    cmd = [CXX, "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(HERE, "cpp", "device_face_run.cpp"), "-L", LIBDIR, "-lcoadapt_b200",
+           "-L", "/usr/local/cuda/lib64", "-lcudart",
+           f"-Wl,-rpath,{LIBDIR}", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
+def test_device_face_run_builds(tmp_path):
+    """the functional C++ program compiles against device.hpp + segments.hpp"""
+    _build_face_run(str(tmp_path / "face_run"))
+
+
+@pytest.mark.gpu
+def test_device_face_sequence_vs_oracle(tmp_path):
+    """INTEGRATION.md §1 from C++ (tests/cpp/device_face_run.cpp): segments
+    from coadapt::gns_segments, d = 1 record_fused (+ record_fused_host and the
+    trainer-form accumulate), d = 2 record_micro_bucket + record_mean_gradient
+    over BucketLayout::slice; the program itself checks the device finalize /
+    EMA / phi bit-identical to the reference API on the host; here every
+    partial and result is checked against the oracle on the same generator."""
+    import json
+    import numpy as np
+    from oracle import oracle as O
+    from paper_2604_26687_b200 import layout as Lay
+    exe = str(tmp_path / "face_run")
+    _build_face_run(exe)
+    M, Bm, seed = 4, 2, 0xFACE
+    unit = Lay.noise_unit_for(256.0, Bm)
+    r = _run(exe, float(unit).hex(), str(seed))
+    assert r.returncode == 0, r.stdout + r.stderr
+    out = json.loads(r.stdout)
+    assert out["host_api_bit_identical"] is True
+    spec = Lay._llama("tiny", 1000, 256, 4, 512, 4, 2, tied=False, qkv_bias=True)
+    lay = Lay.rank_layout(spec, 1, 2, 2, 1)
+    assert out["numel"] == lay.numel and out["counted"] == lay.counted
+    assert any(w == 0.0 for _, _, w in lay.segments)  # dedup gaps present
+
+    # d = 1
+    bufs = [O.synth_fill(lay.numel, O.BF16, lay.gen, seed, m, Lay.G0, unit) for m in range(M)]
+    s, ss = O.fused_sqnorms(bufs, O.BF16, lay.segments, 4)
+    exp = np.append(s, ss / (M * M))
+    for key in ("d1_partials", "d1_host_partials", "accumulate_partials"):
+        got = np.array(out[key])
+        assert np.allclose(got, exp, rtol=1e-9, atol=0), (key, got, exp)
+    st = O.finalize_step(s, ss / (M * M), M * Bm)
+    state = O.State.default()
+    for _ in range(2):
+        O.update_ema(state, st, M * Bm * 2048)
+    res = out["d1_result"]
+    assert res["signal"] == pytest.approx(st.signal, rel=1e-7)
+    assert res["noise"] == pytest.approx(st.noise, rel=1e-7)
+    assert res["b_simple"] == pytest.approx(st.noise / st.signal, rel=1e-7)
+    assert res["phi"] == pytest.approx(O.gns(state), rel=1e-7)
+    assert res["tokens_seen"] == state.tokens_seen
+
+    # d = 2
+    d = 2
+    s2 = [O.sqnorm(O.synth_fill(lay.numel, O.BF16, lay.gen, seed, n, Lay.G0, unit), O.BF16,
+                   lay.segments) for n in range(d * M)]
+    mean = O.synth_mean_fill(lay.numel, O.BF16, lay.gen, seed, 0, d * M, Lay.G0, unit)
+    g2 = O.sqnorm(mean, O.BF16, lay.segments)
+    got = np.array(out["d2_partials"])
+    assert np.allclose(got, np.append(s2, g2), rtol=1e-9, atol=0), (got, s2, g2)
+    st2 = O.finalize_step(s2, g2, d * M * Bm)
+    res2 = out["d2_result"]
+    assert res2["signal"] == pytest.approx(st2.signal, rel=1e-7)
+    assert res2["b_simple"] == pytest.approx(st2.noise / st2.signal, rel=1e-7)
