@@ -30,10 +30,14 @@
  *  - one coadapt_gns per (device, stream); it is not thread-safe, and its
  *    launches share scratch (per-CTA partials, a completion ticket), so all
  *    calls on one coadapt_gns must be ordered on one stream (or streams
- *    joined by events).  Plans are read-only after their first use and may
- *    be shared; their first fused/accumulate use builds a chunk table
- *    (synchronous), so make that first call before any CUDA-graph capture —
- *    after it, begin_step .. finalize are capturable and replayable.
+ *    joined by events).  Plans are read-only after creation and may be
+ *    shared: coadapt_plan_create builds every device table any launch of
+ *    the plan can use (the TMA chunk numbering for every batch size 1..16
+ *    and fused M, the trainer form's whole-bucket table), so no launch
+ *    allocates or copies synchronously and begin_step .. finalize (and
+ *    allreduce_finalize_p2p, whose epoch counter lives in device memory)
+ *    are capturable into a CUDA graph and replayable without an eager
+ *    warm-up call.
  */
 #ifndef COADAPT_CUDA_H
 #define COADAPT_CUDA_H

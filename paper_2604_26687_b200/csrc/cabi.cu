@@ -128,9 +128,14 @@ struct coadapt_plan {
   struct Chunks {
     std::vector<uint64_t> prefix;
     uint64_t* dev = nullptr;
+    bool pooled = false;  // dev points into chunk_pool
   };
   // deque: references stay valid while other P values are added
   std::deque<std::pair<int, Chunks>> chunks;
+  // every table the TMA launches can ask for, uploaded at plan creation in
+  // one allocation (so no launch path allocates or copies synchronously and
+  // a step can be captured into a CUDA graph without an eager warm-up)
+  uint64_t* chunk_pool = nullptr;
   std::mutex mu;  // guards the lazily built tables (chunks, full)
   // whole-bucket table for the trainer form (weight-0 ranges and gaps
   // included, abs == cum); built lazily, not for DP-slice plans
@@ -162,7 +167,6 @@ struct coadapt_gns {
   void* mbox = nullptr;
   int mbox_world = 0, mbox_cap = 0, mbox_rank = -1;
   char* mbox_peers[coadapt::dev::kMaxPeers] = {};
-  uint64_t epoch = 0;
   // host streaming (coadapt_gns_fused_sqnorm_host)
   void* staging = nullptr;  // kStages * 16 * kStageElems * es bytes
   size_t staging_bytes = 0;
@@ -228,6 +232,9 @@ int build_ranges(const coadapt_segment* segs, size_t nseg,
   return COADAPT_OK;
 }
 
+int plan_all_chunks(coadapt_plan* p);
+int plan_full(coadapt_plan* p);
+
 int plan_make(const coadapt_segment* segs, size_t nseg, uint64_t bucket_numel,
               int dtype, int device, uint64_t lo, uint64_t hi,
               coadapt_plan** out) {
@@ -262,6 +269,15 @@ int plan_make(const coadapt_segment* segs, size_t nseg, uint64_t bucket_numel,
       return fail(COADAPT_E_CUDA, std::string("plan upload: ") +
                                       cudaGetErrorString(e));
     }
+    if (int rc = plan_all_chunks(p)) {
+      coadapt_plan_destroy(p);
+      return rc;
+    }
+    if (!p->is_slice)
+      if (int rc = plan_full(p)) {
+        coadapt_plan_destroy(p);
+        return rc;
+      }
   }
   *out = p;
   return COADAPT_OK;
@@ -326,7 +342,53 @@ int launch_fused_window(coadapt_gns* g, const coadapt_plan* p,
   return COADAPT_OK;
 }
 
-// chunk numbering of `p` for chunk size P (built on first use, synchronous)
+std::vector<uint64_t> chunk_prefix(const coadapt_plan* p, int P) {
+  std::vector<uint64_t> prefix(p->host.size() + 1);
+  uint64_t acc = 0;
+  for (size_t k = 0; k < p->host.size(); ++k) {
+    prefix[k] = acc;
+    const uint64_t rb = p->host[k].abs_begin, re = rb + p->host[k].len;
+    acc += (re - 1) / P - rb / P + 1;
+  }
+  prefix.back() = acc;
+  return prefix;
+}
+
+// The chunk numbering for every chunk size P a TMA launch of this plan can
+// use (K1 over 1..16 buckets, K1f for M = 2..16, the host-streaming fused
+// form), built once at plan creation into one device allocation.
+int plan_all_chunks(coadapt_plan* p) {
+  std::vector<int> Ps;
+  for (int M = 1; M <= coadapt::dev::kMaxFusedM; ++M)
+    for (bool mean : {false, true}) {
+      const int P = coadapt::dev::tma_chunk_elems(p->dtype, M, mean);
+      if (P > 0 && std::find(Ps.begin(), Ps.end(), P) == Ps.end()) Ps.push_back(P);
+    }
+  if (Ps.empty()) return COADAPT_OK;
+  const size_t per = p->host.size() + 1;
+  std::vector<uint64_t> all;
+  all.reserve(per * Ps.size());
+  for (int P : Ps) {
+    const auto v = chunk_prefix(p, P);
+    all.insert(all.end(), v.begin(), v.end());
+  }
+  CU(cudaMalloc(&p->chunk_pool, sizeof(uint64_t) * all.size()));
+  CU(cudaMemcpy(p->chunk_pool, all.data(), sizeof(uint64_t) * all.size(),
+                cudaMemcpyHostToDevice));
+  std::lock_guard<std::mutex> lock(p->mu);
+  for (size_t i = 0; i < Ps.size(); ++i) {
+    coadapt_plan::Chunks c;
+    c.prefix.assign(all.begin() + i * per, all.begin() + (i + 1) * per);
+    c.dev = p->chunk_pool + i * per;
+    c.pooled = true;
+    p->chunks.emplace_back(Ps[i], std::move(c));
+  }
+  return COADAPT_OK;
+}
+
+// chunk numbering of `p` for chunk size P: from the tables built at
+// creation; any other P is built here (synchronous; not reached by the
+// library's own launch shapes)
 int plan_chunks(coadapt_plan* p, int P, const coadapt_plan::Chunks** out) {
   std::lock_guard<std::mutex> lock(p->mu);
   for (auto& kv : p->chunks)
@@ -335,14 +397,7 @@ int plan_chunks(coadapt_plan* p, int P, const coadapt_plan::Chunks** out) {
       return COADAPT_OK;
     }
   coadapt_plan::Chunks c;
-  c.prefix.resize(p->host.size() + 1);
-  uint64_t acc = 0;
-  for (size_t k = 0; k < p->host.size(); ++k) {
-    c.prefix[k] = acc;
-    const uint64_t rb = p->host[k].abs_begin, re = rb + p->host[k].len;
-    acc += (re - 1) / P - rb / P + 1;
-  }
-  c.prefix.back() = acc;
+  c.prefix = chunk_prefix(p, P);
   CU(cudaMalloc(&c.dev, sizeof(uint64_t) * c.prefix.size()));
   const cudaError_t e = cudaMemcpy(c.dev, c.prefix.data(),
                                    sizeof(uint64_t) * c.prefix.size(),
@@ -582,7 +637,8 @@ int coadapt_plan_destroy(coadapt_plan* p) {
     if (p->ranges) cudaFree(p->ranges);
     if (p->full) cudaFree(p->full);
     for (auto& kv : p->chunks)
-      if (kv.second.dev) cudaFree(kv.second.dev);
+      if (kv.second.dev && !kv.second.pooled) cudaFree(kv.second.dev);
+    if (p->chunk_pool) cudaFree(p->chunk_pool);
   }
   delete p;
   return COADAPT_OK;
@@ -1175,8 +1231,7 @@ int coadapt_gns_mailbox(coadapt_gns* g, int nranks, void** out) {
     CU(cudaMemset(g->mbox, 0, bytes));
     g->mbox_world = nranks;
     g->mbox_cap = cap;
-    g->mbox_rank = -1;
-    g->epoch = 0;
+    g->mbox_rank = -1;  // (the zeroed mailbox restarts the epoch counter)
   }
   *out = g->mbox;
   return COADAPT_OK;
@@ -1219,7 +1274,6 @@ int coadapt_gns_allreduce_finalize_p2p(coadapt_gns* g, int64_t tokens,
   a.world = g->mbox_world;
   a.rank = g->mbox_rank;
   a.cap = g->mbox_cap;
-  a.epoch = ++g->epoch;
   a.timeout_ns = 10'000'000'000ll;  // a peer 10 s late is a failure, not a hang
   for (int q = 0; q < a.world; ++q) a.mbox[q] = g->mbox_peers[q];
   CU(coadapt::dev::launch_p2p_finalize(a, s));
@@ -1367,11 +1421,23 @@ int coadapt_sqnorm_host(const void* v, uint64_t n, int dtype, int device,
   GUARD(device);
   // bounded device footprint whatever n is (the span overload's host vector
   // may be larger than HBM): fixed 32 Mi-element chunks,
-  // chunk sums added in chunk order on the host in fp64
+  // chunk sums added in chunk order on the host in fp64.  The staging
+  // buffer is kept per device between calls (grown, never shrunk), so a
+  // small span costs one copy and one launch, not an allocation.
   const int es = esize(dtype);
   const uint64_t chunk = std::min<uint64_t>(n, 32ull << 20);
-  void* d = nullptr;
-  CU(cudaMalloc(&d, (size_t)chunk * es));
+  static std::mutex scratch_mu;
+  static std::vector<std::pair<void*, size_t>> scratch;  // per device
+  std::lock_guard<std::mutex> lock(scratch_mu);
+  if ((int)scratch.size() <= device) scratch.resize(device + 1, {nullptr, 0});
+  auto& slot = scratch[device];
+  if (slot.second < (size_t)chunk * es) {
+    if (slot.first) cudaFree(slot.first);
+    slot = {nullptr, 0};
+    CU(cudaMalloc(&slot.first, (size_t)chunk * es));
+    slot.second = (size_t)chunk * es;
+  }
+  void* d = slot.first;
   double total = 0.0;
   int rc = COADAPT_OK;
   for (uint64_t b = 0; b < n && rc == COADAPT_OK; b += chunk) {
@@ -1387,7 +1453,6 @@ int coadapt_sqnorm_host(const void* v, uint64_t n, int dtype, int device,
     rc = coadapt_sqnorm_device(d, k, dtype, device, &part, nullptr);
     total += part;
   }
-  cudaFree(d);
   if (rc == COADAPT_OK) *out = total;
   return rc;
 }

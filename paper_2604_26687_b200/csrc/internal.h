@@ -113,18 +113,20 @@ cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 // this epoch, sums the blocks in rank order (identical bits on every rank)
 // and finalizes.  Mailbox of `world` ranks, `cap` doubles per block:
 //   double data[2][world][cap]; uint64 flags[2][world]   (buffer = epoch & 1)
+//   uint64 epoch   (this rank's step counter, read and advanced by the
+//                   kernel itself, so a CUDA-graph replay moves to the next
+//                   epoch and buffer parity like an eager call)
 constexpr int kMaxPeers = 8;
 struct P2PArgs {
   FinalizeArgs fin;
   double* slots;             // == fin.slots, receives the global sums
   int32_t world, rank, cap;
-  uint64_t epoch;            // >= 1, the same on every rank for one step
   int64_t timeout_ns;
   char* mbox[kMaxPeers];     // rank q's mailbox (peer-mapped; own = local)
 };
 cudaError_t launch_p2p_finalize(const P2PArgs& a, cudaStream_t s);
 inline size_t mailbox_bytes(int world, int cap) {
-  return (size_t)2 * world * cap * sizeof(double) + (size_t)2 * world * 8;
+  return (size_t)2 * world * cap * sizeof(double) + (size_t)2 * world * 8 + 8;
 }
 
 struct GenSeg {

@@ -1224,8 +1224,18 @@ __device__ __forceinline__ uint64_t global_ns() {
 // status-2 result after timeout_ns instead of a hang.
 __global__ void __launch_bounds__(256) p2p_finalize_kernel(const __grid_constant__ P2PArgs a) {
   const int nv = a.fin.n + 1, tid = threadIdx.x;
-  const int buf = (int)(a.epoch & 1);
   const size_t data_doubles = (size_t)2 * a.world * a.cap;
+  // the step counter lives in device memory after this rank's flags: every
+  // launch (eager or a graph replay) takes the next epoch, the same on every
+  // rank because every rank runs the same sequence of steps
+  uint64_t* ctr = reinterpret_cast<uint64_t*>(
+                      reinterpret_cast<double*>(a.mbox[a.rank]) + data_doubles) +
+                  2 * a.world;
+  __shared__ uint64_t s_epoch;
+  if (tid == 0) s_epoch = *ctr + 1;
+  __syncthreads();
+  const uint64_t epoch = s_epoch;
+  const int buf = (int)(epoch & 1);
   for (int q = 0; q < a.world; ++q) {
     double* dst = reinterpret_cast<double*>(a.mbox[q]) +
                   ((size_t)buf * a.world + a.rank) * a.cap;
@@ -1238,7 +1248,7 @@ __global__ void __launch_bounds__(256) p2p_finalize_kernel(const __grid_constant
       uint64_t* f = reinterpret_cast<uint64_t*>(
                         reinterpret_cast<double*>(a.mbox[q]) + data_doubles) +
                     buf * a.world + a.rank;
-      st_release_sys(f, a.epoch);
+      st_release_sys(f, epoch);
     }
   }
   __shared__ int timed_out;
@@ -1248,7 +1258,7 @@ __global__ void __launch_bounds__(256) p2p_finalize_kernel(const __grid_constant
   const uint64_t* flags = reinterpret_cast<const uint64_t*>(mine + data_doubles);
   if (tid < a.world) {
     const uint64_t t0 = global_ns();
-    while (ld_acquire_sys(flags + buf * a.world + tid) < a.epoch) {
+    while (ld_acquire_sys(flags + buf * a.world + tid) < epoch) {
       if ((int64_t)(global_ns() - t0) > a.timeout_ns) {
         atomicExch(&timed_out, 1);
         break;
@@ -1258,6 +1268,7 @@ __global__ void __launch_bounds__(256) p2p_finalize_kernel(const __grid_constant
     __threadfence_system();  // order this thread's acquire before the CTA's reads
   }
   __syncthreads();
+  if (tid == 0) *ctr = epoch;  // nothing else in this launch reads it again
   if (timed_out) {
     if (tid == 0) {
       DevResult* res = static_cast<DevResult*>(a.fin.result);

@@ -34,8 +34,15 @@
 #include <cstring>
 #include <string>
 
+#include <poll.h>
+#include <sys/socket.h>
 #include <sys/syscall.h>
+#include <sys/un.h>
 #include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <thread>
 
 #include "../../include/coadapt_cuda.h"
 
@@ -258,6 +265,105 @@ int coadapt_nvls_create(int device, int nranks, uint64_t bytes, coadapt_nvls** o
   return COADAPT_OK;
 }
 
+namespace {
+
+// The multicast handle is a POSIX fd; it reaches the other ranks the way
+// NCCL passes its cuMem handles: over a Unix domain socket as SCM_RIGHTS
+// ancillary data.  The exporter listens on an abstract-namespace socket
+// named after (pid, fd, nonce) and serves the fd to nranks-1 importers from
+// a detached thread (its own dup of the fd, 300 s deadline).  pidfd_getfd
+// stays as the fallback for importers that cannot reach the socket; it
+// needs ptrace rights over the exporter (Yama ptrace_scope / CAP_SYS_PTRACE).
+void sock_name(sockaddr_un& a, socklen_t& len, int32_t pid, int32_t fd, int32_t nonce) {
+  std::memset(&a, 0, sizeof(a));
+  a.sun_family = AF_UNIX;
+  const int n = std::snprintf(a.sun_path + 1, sizeof(a.sun_path) - 1,
+                              "coadapt-nvls-%d-%d-%d", pid, fd, nonce);
+  len = (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + n);
+}
+
+int serve_fd(int fd, int32_t pid, int32_t nonce, int clients) {
+  const int ls = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+  if (ls < 0) return -1;
+  sockaddr_un a;
+  socklen_t len;
+  sock_name(a, len, pid, fd, nonce);
+  if (bind(ls, reinterpret_cast<sockaddr*>(&a), len) != 0 || listen(ls, clients) != 0) {
+    close(ls);
+    return -1;
+  }
+  const int mine = dup(fd);
+  std::thread([ls, mine, clients] {
+    const auto end = std::chrono::steady_clock::now() + std::chrono::seconds(300);
+    for (int served = 0; served < clients;) {
+      const auto left = std::chrono::duration_cast<std::chrono::milliseconds>(
+          end - std::chrono::steady_clock::now()).count();
+      if (left <= 0) break;
+      pollfd pf{ls, POLLIN, 0};
+      if (poll(&pf, 1, (int)std::min<long long>(left, 1000)) <= 0) continue;
+      const int c = accept4(ls, nullptr, nullptr, SOCK_CLOEXEC);
+      if (c < 0) continue;
+      char byte = 'F';
+      iovec iov{&byte, 1};
+      alignas(cmsghdr) char ctl[CMSG_SPACE(sizeof(int))];
+      std::memset(ctl, 0, sizeof(ctl));
+      msghdr m;
+      std::memset(&m, 0, sizeof(m));
+      m.msg_iov = &iov;
+      m.msg_iovlen = 1;
+      m.msg_control = ctl;
+      m.msg_controllen = sizeof(ctl);
+      cmsghdr* cm = CMSG_FIRSTHDR(&m);
+      cm->cmsg_level = SOL_SOCKET;
+      cm->cmsg_type = SCM_RIGHTS;
+      cm->cmsg_len = CMSG_LEN(sizeof(int));
+      std::memcpy(CMSG_DATA(cm), &mine, sizeof(int));
+      if (sendmsg(c, &m, MSG_NOSIGNAL) == 1) ++served;
+      close(c);
+    }
+    close(ls);
+    close(mine);
+  }).detach();
+  return 0;
+}
+
+// fd from the exporter's socket, or -1 (caller falls back to pidfd_getfd)
+int receive_fd(int32_t pid, int32_t fd, int32_t nonce) {
+  sockaddr_un a;
+  socklen_t len;
+  sock_name(a, len, pid, fd, nonce);
+  for (int attempt = 0; attempt < 100; ++attempt) {  // ~5 s: the server may lag
+    const int c = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+    if (c < 0) return -1;
+    if (connect(c, reinterpret_cast<sockaddr*>(&a), len) == 0) {
+      char byte = 0;
+      iovec iov{&byte, 1};
+      alignas(cmsghdr) char ctl[CMSG_SPACE(sizeof(int))];
+      msghdr m;
+      std::memset(&m, 0, sizeof(m));
+      m.msg_iov = &iov;
+      m.msg_iovlen = 1;
+      m.msg_control = ctl;
+      m.msg_controllen = sizeof(ctl);
+      int got = -1;
+      if (recvmsg(c, &m, MSG_CMSG_CLOEXEC) == 1) {
+        for (cmsghdr* cm = CMSG_FIRSTHDR(&m); cm; cm = CMSG_NXTHDR(&m, cm))
+          if (cm->cmsg_level == SOL_SOCKET && cm->cmsg_type == SCM_RIGHTS)
+            std::memcpy(&got, CMSG_DATA(cm), sizeof(int));
+      }
+      close(c);
+      return got;
+    }
+    close(c);
+    std::this_thread::sleep_for(std::chrono::milliseconds(50));
+  }
+  return -1;
+}
+
+std::atomic<int32_t> g_nonce{1};
+
+}  // namespace
+
 int coadapt_nvls_export(const coadapt_nvls* o, void* handle, size_t len) {
   if (!o || !handle || len < 64)
     return fail(COADAPT_E_VALIDATION, "need an object and a >= 64-byte handle buffer");
@@ -268,6 +374,8 @@ int coadapt_nvls_export(const coadapt_nvls* o, void* handle, size_t len) {
   blob[0] = 0x4e564c53;  // "NVLS"
   blob[1] = (int32_t)getpid();
   blob[2] = fd;  // stays open in the exporting process for the importers
+  blob[3] = g_nonce.fetch_add(1) ^ (int32_t)(uintptr_t)o;
+  blob[4] = serve_fd(fd, blob[1], blob[3], o->nranks - 1) == 0 ? 1 : 0;  // socket served
   if (o->export_fd >= 0) close(o->export_fd);
   o->export_fd = fd;
   std::memcpy(handle, blob, sizeof(blob));
@@ -283,12 +391,24 @@ int coadapt_nvls_import(int device, int nranks, uint64_t bytes, const void* hand
   int32_t blob[16];
   std::memcpy(blob, handle, sizeof(blob));
   if (blob[0] != 0x4e564c53) return fail(COADAPT_E_VALIDATION, "not an NVLS handle");
-  // duplicate the exporter's descriptor into this process
-  const int pidfd = (int)syscall(434 /* pidfd_open */, (pid_t)blob[1], 0);
-  if (pidfd < 0) return fail(COADAPT_E_CUDA, "pidfd_open of the exporting rank failed");
-  const int fd = (int)syscall(438 /* pidfd_getfd */, pidfd, blob[2], 0);
-  close(pidfd);
-  if (fd < 0) return fail(COADAPT_E_CUDA, "pidfd_getfd of the multicast handle failed");
+  // the exporter's descriptor: SCM_RIGHTS over its socket, else pidfd_getfd
+  // (COADAPT_NVLS_SHARE=socket|pidfd forces one path, for tests)
+  const char* force = getenv("COADAPT_NVLS_SHARE");
+  const bool only_socket = force && std::string(force) == "socket";
+  const bool only_pidfd = force && std::string(force) == "pidfd";
+  int fd = (blob[4] && !only_pidfd) ? receive_fd(blob[1], blob[2], blob[3]) : -1;
+  if (fd < 0 && only_socket)
+    return fail(COADAPT_E_CUDA, "SCM_RIGHTS transfer of the multicast handle failed");
+  if (fd < 0) {
+    const int pidfd = (int)syscall(434 /* pidfd_open */, (pid_t)blob[1], 0);
+    if (pidfd < 0) return fail(COADAPT_E_CUDA, "pidfd_open of the exporting rank failed");
+    fd = (int)syscall(438 /* pidfd_getfd */, pidfd, blob[2], 0);
+    close(pidfd);
+    if (fd < 0)
+      return fail(COADAPT_E_CUDA,
+                  "neither the exporter's socket (SCM_RIGHTS) nor pidfd_getfd delivered "
+                  "the multicast handle");
+  }
   DevScope scope(device);
   CUmulticastObjectProp p = mc_prop(nranks, bytes);
   size_t gran = 0;

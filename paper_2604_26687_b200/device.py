@@ -30,6 +30,33 @@ def _ptr(x) -> int:
     return int(x)
 
 
+def _bucket(plan: "BucketPlan", x, what: str = "bucket", host: bool = False) -> int:
+    """Pointer of a bucket for `plan`, validated when it is a tensor: the
+    plan's dtype, contiguous, at least bucket_numel elements, on the plan's
+    GPU (host=False) or in host memory (host=True).  Raw addresses (ints,
+    e.g. CUDA-IPC peer pointers) are the caller's responsibility."""
+    if isinstance(x, torch.Tensor):
+        want = DTYPE_TO_TORCH[plan.dtype]
+        if x.dtype != want:
+            raise L.ValidationError(f"{what}: dtype {x.dtype}, the plan is {want}")
+        if not x.is_contiguous():
+            raise L.ValidationError(f"{what}: not contiguous")
+        if x.numel() < plan.bucket_numel:
+            raise L.ValidationError(f"{what}: {x.numel()} elements < the plan's bucket_numel "
+                                    f"{plan.bucket_numel}")
+        if host:
+            if x.is_cuda:
+                raise L.ValidationError(f"{what}: expected host memory, got {x.device}")
+        elif not x.is_cuda or x.device.index != plan.device:
+            raise L.ValidationError(f"{what}: on {x.device}, the plan is on cuda:{plan.device}")
+        return x.data_ptr()
+    if host and hasattr(x, "ctypes"):
+        if x.size < plan.bucket_numel or x.itemsize != ESIZE[plan.dtype]:
+            raise L.ValidationError(f"{what}: host array smaller than the plan or wrong element size")
+        return x.ctypes.data
+    return int(x)
+
+
 def _host_ptr(x) -> int:
     if isinstance(x, torch.Tensor):
         return x.data_ptr()
@@ -126,13 +153,13 @@ class GnsDevice:
         check(lib().coadapt_gns_begin_step(self.handle, _stream(stream)))
 
     def micro_sqnorm(self, plan: BucketPlan, bucket, dp_index: int, micro: int, stream=None) -> None:
-        check(lib().coadapt_gns_micro_sqnorm(self.handle, plan.handle, _ptr(bucket), int(dp_index),
+        check(lib().coadapt_gns_micro_sqnorm(self.handle, plan.handle, _bucket(plan, bucket), int(dp_index),
                                              int(micro), _stream(stream)))
 
     def micro_sqnorm_batched(self, plan: BucketPlan, buckets: Sequence, dp_index: Sequence[int],
                              micro: Sequence[int], stream=None) -> None:
         k = len(buckets)
-        ptrs = (C.c_void_p * max(1, k))(*[_ptr(b) for b in buckets])
+        ptrs = (C.c_void_p * max(1, k))(*[_bucket(plan, b) for b in buckets])
         di = (C.c_int32 * max(1, k))(*dp_index)
         mi = (C.c_int32 * max(1, k))(*micro)
         check(lib().coadapt_gns_micro_sqnorm_batched(self.handle, plan.handle, ptrs, di, mi, k,
@@ -140,23 +167,25 @@ class GnsDevice:
 
     def fused_sqnorm(self, plan: BucketPlan, buckets: Sequence, stream=None) -> None:
         k = len(buckets)
-        ptrs = (C.c_void_p * max(1, k))(*[_ptr(b) for b in buckets])
+        ptrs = (C.c_void_p * max(1, k))(*[_bucket(plan, b) for b in buckets])
         check(lib().coadapt_gns_fused_sqnorm(self.handle, plan.handle, ptrs, k, _stream(stream)))
 
     def fused_sqnorm_host(self, plan: BucketPlan, host_buckets: Sequence, stream=None) -> None:
         k = len(host_buckets)
-        ptrs = (C.c_void_p * max(1, k))(*[_ptr(b) if isinstance(b, torch.Tensor) else b.ctypes.data
+        ptrs = (C.c_void_p * max(1, k))(*[_bucket(plan, b, "host bucket", host=True)
                                           for b in host_buckets])
         check(lib().coadapt_gns_fused_sqnorm_host(self.handle, plan.handle, ptrs, k, _stream(stream)))
 
     def micro_sqnorm_host(self, plan: BucketPlan, host_bucket, dp_index: int, micro: int,
                           stream=None) -> None:
         """K1 over a host (ideally pinned) bucket, streamed H2D."""
-        check(lib().coadapt_gns_micro_sqnorm_host(self.handle, plan.handle, _host_ptr(host_bucket),
+        check(lib().coadapt_gns_micro_sqnorm_host(self.handle, plan.handle,
+                                                  _bucket(plan, host_bucket, "host bucket", host=True),
                                                   int(dp_index), int(micro), _stream(stream)))
 
     def mean_sqnorm_host(self, plan: BucketPlan, host_mean, stream=None) -> None:
-        check(lib().coadapt_gns_mean_sqnorm_host(self.handle, plan.handle, _host_ptr(host_mean),
+        check(lib().coadapt_gns_mean_sqnorm_host(self.handle, plan.handle,
+                                                 _bucket(plan, host_mean, "host mean", host=True),
                                                  _stream(stream)))
 
     ACC_FIRST, ACC_LAST_MEAN = 1, 2
@@ -168,11 +197,16 @@ class GnsDevice:
         last micro-batch of a d == 1 step, gbar^2) fused in."""
         if main_grad.dtype != torch.float32:
             raise L.ValidationError("main_grad must be fp32")
+        if not main_grad.is_contiguous() or main_grad.numel() < plan.bucket_numel or \
+                not main_grad.is_cuda or main_grad.device.index != plan.device:
+            raise L.ValidationError("main_grad: contiguous fp32 on the plan's GPU with at least "
+                                    "bucket_numel elements")
         flags = (self.ACC_FIRST if first else 0) | (self.ACC_LAST_MEAN if last_mean else 0)
         if mean_scale_sq is None:
             mean_scale_sq = 1.0 / float(self.micro_count) ** 2
         check(lib().coadapt_gns_accumulate(self.handle, plan.handle, main_grad.data_ptr(),
-                                           _ptr(micro_grad), int(dp_index), int(micro), flags,
+                                           _bucket(plan, micro_grad, "micro_grad"), int(dp_index),
+                                           int(micro), flags,
                                            float(mean_scale_sq), _stream(stream)))
 
     def barrier(self, stream=None) -> None:
@@ -184,7 +218,7 @@ class GnsDevice:
         """Fused DP reduce-scatter + gbar^2 over NVLink (peer pointers from
         ipc_open; the local replica by pointer)."""
         k = len(replicas)
-        ptrs = (C.c_void_p * max(1, k))(*[_ptr(r) for r in replicas])
+        ptrs = (C.c_void_p * max(1, k))(*[_bucket(plan, r, "replica") for r in replicas])
         check(lib().coadapt_gns_reduce_scatter_sqnorm(self.handle, plan.handle, ptrs, k, int(dp_rank),
                                                       _ptr(out_slice), float(scale), _stream(stream)))
 
@@ -193,12 +227,13 @@ class GnsDevice:
         """All-reduce form: the synchronised slice is written back into every
         replica (in place, peers' over NVLink) and its gbar^2 accumulated."""
         k = len(replicas)
-        ptrs = (C.c_void_p * max(1, k))(*[_ptr(r) for r in replicas])
+        ptrs = (C.c_void_p * max(1, k))(*[_bucket(plan, r, "replica") for r in replicas])
         check(lib().coadapt_gns_allreduce_sqnorm(self.handle, plan.handle, ptrs, k, int(dp_rank),
                                                  float(scale), _stream(stream)))
 
     def mean_sqnorm(self, plan: BucketPlan, mean_grad, stream=None) -> None:
-        check(lib().coadapt_gns_mean_sqnorm(self.handle, plan.handle, _ptr(mean_grad), _stream(stream)))
+        check(lib().coadapt_gns_mean_sqnorm(self.handle, plan.handle, _bucket(plan, mean_grad, "mean_grad"),
+                                            _stream(stream)))
 
     def attach_nccl(self, nranks: int, rank: int, unique_id: bytes) -> None:
         buf = C.create_string_buffer(bytes(unique_id), len(unique_id))

@@ -44,6 +44,63 @@ def run_job(g, lays, ranks, M, d, seed, unit, fused):
             g.mean_sqnorm(sl, mean)
 
 
+def graph_p2p_case(lays, mine, M, d, unit, local, world, rank):
+    """X1 + K3 over NVLink captured in a CUDA graph (no eager warm-up: the
+    plans built their tables at creation) and replayed on fresh data each
+    step: every replay must move to the next mailbox epoch, so its phi and
+    slots equal an eager NCCL step on the same data."""
+    gg = D.GnsDevice(d, M, d * M, local)
+    bases = Dist.attach_p2p(gg, dist, world, rank)
+    ge = D.GnsDevice(d, M, d * M, local)
+    Dist.attach(ge, dist, world, rank)
+    s = torch.cuda.Stream()
+    bufs = {vr: [torch.empty(lays[vr].numel, dtype=torch.bfloat16, device="cuda") for _ in range(M)]
+            for vr in mine}
+    plans = {vr: D.BucketPlan(lays[vr].segments, lays[vr].numel, L.BF16, local) for vr in mine}
+
+    def fill(k):
+        for vr in mine:
+            i_d = lays[vr].coords[0]
+            for m in range(M):
+                D.synth_fill(bufs[vr][m], lays[vr].gen, 0xC0905 + k, i_d * M + m, Lay.G0, unit, s)
+
+    def body(g):
+        g.begin_step(s)
+        for vr in mine:
+            i_d = lays[vr].coords[0]
+            g.micro_sqnorm_batched(plans[vr], bufs[vr], [i_d] * M, list(range(M)), s)
+            # the d > 1 mean term is not part of this check: K1 slots only
+    tokens = d * M * 2048
+    torch.cuda.synchronize()
+    dist.barrier()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        body(gg)
+        gg.allreduce_finalize_p2p(tokens, s)
+    good, worst = True, 0.0
+    for k in range(1, 5):
+        with torch.cuda.stream(s):
+            fill(k)
+            graph.replay()
+        rg = gg.result()
+        pg = gg.partials()
+        body(ge)
+        ge.allreduce(s)
+        ge.finalize(tokens, s)
+        re = ge.result()
+        pe = ge.partials()
+        rel = float(np.max(np.abs(pg[:-1] - pe[:-1]) / np.abs(pe[:-1])))
+        worst = max(worst, rel)
+        good = good and rg.status == 0 and rel <= 1e-13 and \
+            abs(rg.state.ema_signal - re.state.ema_signal) <= 1e-12 * abs(re.state.ema_signal) and \
+            rg.state.tokens_seen == re.state.tokens_seen == k * tokens
+    torch.cuda.synchronize()
+    dist.barrier()
+    for b in bases:
+        D.ipc_close(b)
+    return {"graph_p2p_replays": 4, "graph_p2p_max_rel_slots": worst, "graph_p2p_ok": bool(good)}
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -116,6 +173,9 @@ def main():
             torch.cuda.synchronize()
             case[f"tail_us_{name}"] = e0.elapsed_time(e1) / 50 * 1e3
         dist.barrier()
+        if (d, t, p) == (2, 2, 2):
+            case.update(graph_p2p_case(lays, mine, M, d, unit, local, world, rank))
+            ok = ok and case["graph_p2p_ok"]
         for b in bases:
             D.ipc_close(b)
         report["cases"].append(case)

@@ -260,3 +260,24 @@ def test_record_reconfig_spec_examples(G):
         cost = G.record_reconfig(c, lat, cost)
         o = O.record_reconfig(*o, lat)
         assert (c.elapsed, c.useful, c.reconfig_total, c.reconfigs, cost) == o
+
+
+def test_python_wrappers_validate_bucket_tensors():
+    """tensors handed to the device wrappers are checked against
+    the plan (dtype, contiguity, element count, device) before any launch."""
+    import types
+    import torch
+    from paper_2604_26687_b200 import device as D
+    from paper_2604_26687_b200 import _lib as LL
+    plan = types.SimpleNamespace(dtype=LL.BF16, bucket_numel=64, device=0)
+    with pytest.raises(LL.ValidationError, match="dtype"):
+        D._bucket(plan, torch.zeros(64, dtype=torch.float32))
+    with pytest.raises(LL.ValidationError, match="contiguous"):
+        D._bucket(plan, torch.zeros(128, dtype=torch.bfloat16)[::2])
+    with pytest.raises(LL.ValidationError, match="elements"):
+        D._bucket(plan, torch.zeros(63, dtype=torch.bfloat16))
+    with pytest.raises(LL.ValidationError, match="cuda:0"):
+        D._bucket(plan, torch.zeros(64, dtype=torch.bfloat16))  # host tensor, device plan
+    host = torch.zeros(64, dtype=torch.bfloat16)
+    assert D._bucket(plan, host, host=True) == host.data_ptr()
+    assert D._bucket(plan, 1234) == 1234  # raw (e.g. CUDA-IPC) addresses pass through

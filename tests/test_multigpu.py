@@ -219,7 +219,9 @@ def test_nvls_switch_reduced_allreduce():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29700 + os.getpid() % 90),
            os.path.join(HERE, "mp_nvls_worker.py")]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    # the multicast handle must travel by SCM_RIGHTS (no pidfd_getfd fallback)
+    env = dict(os.environ, COADAPT_NVLS_SHARE="socket")
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     rep = json.loads(lines[-1])
