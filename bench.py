@@ -51,8 +51,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--x1", choices=["nccl", "p2p"], default="nccl",
-                    help="slot all-reduce: NCCL, or fused with finalize over NVLink mailboxes")
+    ap.add_argument("--x1", choices=["nccl", "p2p"], default="p2p",
+                    help="N > 1 slot all-reduce: fused with finalize over NVLink mailboxes "
+                         "(default), or NCCL all-reduce + finalize")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-elems", type=int, default=128 << 20, help="sample elements per micro-bucket")
     return ap.parse_args()
@@ -285,6 +286,11 @@ def run_ours(args):
     from paper_2604_26687_b200 import layout as Lay
 
     ws, rank, local = dist_env()
+    if ws > 1:
+        # keep NCCL's communicator init lines (one per rank, "nRanks N") in
+        # the log so the rank count of the run is checkable
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     dist = init_dist(ws, "nccl")
     torch.cuda.set_device(local)
     dev = local
@@ -438,9 +444,37 @@ def run_ours(args):
         dist.all_gather(cg, ct)
         if clk is not None:
             clk["sm_mhz_per_gpu"] = [float(x.item()) for x in cg]
+    # the tail on its own: all ranks aligned by a barrier + sync first, so
+    # the number is the exchange + finalize latency without the wait for the
+    # slowest GPU's reductions (that wait is rank_skew_ms)
+    synced = []
+    for _ in range(20 if ws > 1 else 5):
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        if args.x1 == "p2p" and ws > 1:
+            g.allreduce_finalize_p2p(B_g * SEQ_LEN, stream)
+        else:
+            g.allreduce(stream)
+            g.finalize(B_g * SEQ_LEN, stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        synced.append(a0.elapsed_time(a1))
+    synced_ms = statistics.median(synced)
+    if ws > 1:
+        tt = torch.tensor([synced_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        synced_ms = float(tt.item())
     goodput_step = {"step_ms": round(ms, 4), "reductions_ms": round(red_ms, 4),
                     "reductions_ms_per_gpu": [round(x, 4) for x in red_all],
+                    "rank_skew_ms": round(max(red_all) - min(red_all), 4),
                     "allreduce_finalize_ms": round(tail_ms, 4),
+                    "allreduce_finalize_ms_synced": round(synced_ms, 4),
+                    "x1": (("p2p: slot exchange + finalize in one kernel over NVLink"
+                            if args.x1 == "p2p" else "nccl all-reduce + finalize kernel")
+                           if ws > 1 else "local (one GPU)"),
                     "decide_ms": round(1e3 * sum(decide_s) / max(1, len(decide_s)), 4),
                     "candidates": len(cands)}
 

@@ -103,7 +103,7 @@ def test_nccl_two_gpus_matches_one_gpu():
     if n < 2:
         pytest.skip("needs >= 2 GPUs (gpurun --gpus 2)")
     world = 4 if n >= 4 else 2
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 400),
            os.path.join(HERE, "mp_gns_worker.py")]
@@ -111,6 +111,10 @@ def test_nccl_two_gpus_matches_one_gpu():
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     rep = json.loads(lines[-1])
+    print(json.dumps(rep))
+    # NCCL's communicator init lines (NCCL_DEBUG=INFO) prove the rank count
+    print("\n".join(l for l in r.stdout.splitlines() + r.stderr.splitlines()
+                    if "comm" in l and "nRanks" in l))
     assert rep["ok"], rep
 
 
