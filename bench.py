@@ -289,8 +289,9 @@ def run_ours(args):
     if ws > 1:
         # keep NCCL's communicator init lines (one per rank, "nRanks N") in
         # the log so the rank count of the run is checkable
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
     dist = init_dist(ws, "nccl")
     torch.cuda.set_device(local)
     dev = local
