@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--x1", choices=["nccl", "p2p"], default="p2p",
                     help="N > 1 slot all-reduce: fused with finalize over NVLink mailboxes "
                          "(default), or NCCL all-reduce + finalize")
+    ap.add_argument("--finalize", choices=["inpass", "separate"], default="inpass",
+                    help="finalize (and the N > 1 slot exchange) in the last reduction's "
+                         "last CTA (default), or as its own launch(es) after it")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-elems", type=int, default=128 << 20, help="sample elements per micro-bucket")
     return ap.parse_args()
@@ -357,31 +360,46 @@ def run_ours(args):
 
     ev_pairs, tail_pairs, decide_s = [], [], []
 
+    # in-pass: the step's last reduction launch finalizes in its last CTA
+    # (after the NVLink slot exchange when N > 1) — north_star item 2
+    inpass = args.finalize == "inpass" and (ws == 1 or args.x1 == "p2p")
+    tokens = B_g * SEQ_LEN
+
     def step(timed):
         g.begin_step(stream)
         for i, pl in enumerate(plans):
+            last = inpass and i + 1 == len(plans)
             if timed:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
             if fused:
-                g.fused_sqnorm(pl, pool, stream)
+                if last:
+                    g.fused_sqnorm_finalize(pl, pool, tokens, stream)
+                else:
+                    g.fused_sqnorm(pl, pool, stream)
             else:
                 g.micro_sqnorm_batched(pl, pool, [mine[i].coords[0]] * M, list(range(M)), stream)
             if timed:
                 e1.record(stream)
-                ev_pairs.append((e0, e1, launch_bytes[i]))
+                # the launch that also waits for the peers' slots (N > 1) is
+                # kept out of the kernel roofline
+                ev_pairs.append((e0, e1, launch_bytes[i], not (last and fused and ws > 1)))
             if not fused:
-                g.mean_sqnorm(slices[i], mean, stream)
+                if last:
+                    g.mean_sqnorm_finalize(slices[i], mean, tokens, stream)
+                else:
+                    g.mean_sqnorm(slices[i], mean, stream)
         if timed:
             f0 = torch.cuda.Event(enable_timing=True)
             f1 = torch.cuda.Event(enable_timing=True)
             f0.record(stream)
-        if args.x1 == "p2p" and ws > 1:
-            g.allreduce_finalize_p2p(B_g * SEQ_LEN, stream)
-        else:
-            g.allreduce(stream)
-            g.finalize(B_g * SEQ_LEN, stream)
+        if not inpass:
+            if args.x1 == "p2p" and ws > 1:
+                g.allreduce_finalize_p2p(tokens, stream)
+            else:
+                g.allreduce(stream)
+                g.finalize(tokens, stream)
         if timed:
             f1.record(stream)
             tail_pairs.append((f0, f1))
@@ -432,7 +450,7 @@ def run_ours(args):
 
     # C5 "full goodput step" latency split: the reductions,
     # the all-reduce + finalize tail on the device, the host decide()
-    red_ms = sum(a.elapsed_time(b) for a, b, _ in ev_pairs) / args.steps
+    red_ms = sum(a.elapsed_time(b) for a, b, _, _ in ev_pairs) / args.steps
     tail_ms = sum(a.elapsed_time(b) for a, b in tail_pairs) / max(1, len(tail_pairs))
     red_all = [red_ms]
     if ws > 1:  # per-GPU reduction time: the max-over-ranks step waits for the slowest
@@ -476,12 +494,18 @@ def run_ours(args):
                     "x1": (("p2p: slot exchange + finalize in one kernel over NVLink"
                             if args.x1 == "p2p" else "nccl all-reduce + finalize kernel")
                            if ws > 1 else "local (one GPU)"),
+                    "finalize": ("in-pass: in the last CTA of the step's last reduction launch"
+                                 + (" after the NVLink slot exchange" if ws > 1 else "")
+                                 + "; allreduce_finalize_ms measures only the host-side gap "
+                                   "after it, allreduce_finalize_ms_synced the standalone "
+                                   "exchange + finalize kernel" if inpass else "separate launches"),
                     "decide_ms": round(1e3 * sum(decide_s) / max(1, len(decide_s)), 4),
                     "candidates": len(cands)}
 
     # dominant-kernel roofline (per-launch CUDA events on the launching stream)
-    durs = [a.elapsed_time(b) / 1e3 for a, b, _ in ev_pairs]
-    byts = [x for _, _, x in ev_pairs]
+    kept = [e for e in ev_pairs if e[3]] or ev_pairs
+    durs = [a.elapsed_time(b) / 1e3 for a, b, _, _ in kept]
+    byts = [x for _, _, x, _ in kept]
     achieved = sum(byts) / sum(durs) / 1e9
     peak, peak_kind = read_peak()
     kname = "fused_tma_kernel (K1f)" if fused else "fused_tma_kernel<MEAN=false> (K1 on the TMA ring)"

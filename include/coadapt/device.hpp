@@ -71,6 +71,16 @@ class GnsDevicePlan {
                     std::span<const void* const> buckets, void* stream);
   void record_mean_gradient(const BucketLayout& layout, const void* mean,
                             void* stream);
+  // The step's last reduction with the finalize in the same pass (and the
+  // NVLink slot exchange first when mailboxes are attached): replaces the
+  // allreduce + finalize calls that would follow it.
+  void record_fused_finalize(const BucketLayout& layout,
+                             std::span<const void* const> buckets,
+                             std::int64_t tokens_this_step, void* stream);
+  void record_mean_gradient_finalize(const BucketLayout& layout,
+                                     const void* mean,
+                                     std::int64_t tokens_this_step,
+                                     void* stream);
   // The same three with the buckets in HOST memory (pinned for overlap),
   // streamed H2D through the plan's staging ring; buffers must stay valid
   // until the stream work completes.

@@ -337,6 +337,25 @@ int coadapt_gns_allreduce_finalize_p2p(coadapt_gns* g, int64_t tokens,
  * gns.hpp:49, update_ema gns.hpp:67-68, gns gns.hpp:73. */
 int coadapt_gns_finalize(coadapt_gns* g, int64_t tokens_this_step,
                          void* stream);
+
+/* The step's last reduction with the finalize in the same pass (north_star
+ * item 2; Alg. 1): coadapt_gns_fused_sqnorm (d == 1) or
+ * coadapt_gns_mean_sqnorm (d > 1, the last DP slice this rank reads), whose
+ * last CTA, after combining the partials, runs finalize_step + update_ema +
+ * gns — and first, when NVLink mailboxes are attached
+ * (coadapt_gns_attach_mailboxes, world > 1), the slot exchange of
+ * coadapt_gns_allreduce_finalize_p2p.  Replaces that call (or allreduce +
+ * finalize) after the step's last reduction: one launch fewer per step,
+ * identical results.  The result is copied to pinned memory as by
+ * coadapt_gns_finalize.  Validation error for a gns with a multi-rank NCCL
+ * communicator and no mailboxes (use allreduce + finalize there). */
+int coadapt_gns_fused_sqnorm_finalize(coadapt_gns* g, const coadapt_plan* p,
+                                      const void* const* buckets,
+                                      int micro_count, int64_t tokens_this_step,
+                                      void* stream);
+int coadapt_gns_mean_sqnorm_finalize(coadapt_gns* g, const coadapt_plan* p,
+                                     const void* mean_grad,
+                                     int64_t tokens_this_step, void* stream);
 /* waits for the last finalize and returns its result */
 int coadapt_gns_read_result(coadapt_gns* g, coadapt_gns_result* out);
 /* synchronous read of the N+1 slots (s values, then gbar^2) */

@@ -209,6 +209,8 @@ SIGNATURES = {
     "coadapt_gns_attach_nccl": (I, [P, I, I, P, SZ]),
     "coadapt_gns_allreduce": (I, [P, P]),
     "coadapt_gns_finalize": (I, [P, I64, P]),
+    "coadapt_gns_fused_sqnorm_finalize": (I, [P, P, P, I, I64, P]),
+    "coadapt_gns_mean_sqnorm_finalize": (I, [P, P, P, I64, P]),
     "coadapt_gns_read_result": (I, [P, P]),
     "coadapt_gns_read_partials": (I, [P, P, SZ]),
     "coadapt_gns_get_state": (I, [P, P]),

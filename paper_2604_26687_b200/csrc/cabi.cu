@@ -465,19 +465,30 @@ bool use_tma_path() {
   return !(e && std::string(e) == "ldg");
 }
 
+// the finalize tail as its own launch (when no TMA launch could carry it)
+int launch_tail_separately(const coadapt::dev::Tail& t, cudaStream_t s) {
+  if (t.mode == 2)
+    CU(coadapt::dev::launch_p2p_finalize(t.p2p, s));
+  else
+    CU(coadapt::dev::launch_finalize(t.p2p.fin, s));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return COADAPT_OK;
+}
+
 int launch_fused_tma_all(coadapt_gns* g, coadapt_plan* p, const FusedArgs& fa,
-                         int M, cudaStream_t s) {
+                         int M, cudaStream_t s,
+                         const coadapt::dev::Tail* tail = nullptr) {
   const int P = coadapt::dev::tma_chunk_elems(p->dtype, M, fa.gslot >= 0);
   if (P <= 0) return fail(COADAPT_E_INTERNAL, "no TMA kernel for this dtype/M");
   const coadapt_plan::Chunks* ch = nullptr;
   if (int rc = plan_chunks(p, P, &ch)) return rc;
   const uint64_t nch = ch->prefix.back();
-  if (nch == 0) return COADAPT_OK;
+  if (nch == 0) return tail ? launch_tail_separately(*tail, s) : COADAPT_OK;
   const int grid = (int)std::min<uint64_t>(std::max(1, g->sms), nch);
   if (int rc = ensure_partials(g, (size_t)grid * (M + 1))) return rc;
   Sink sink{g->partials, g->ticket, g->slots};
   CU(coadapt::dev::launch_fused_tma(p->dtype, M, p->ranges, (int)p->host.size(),
-                                    ch->dev, 0, nch, fa, sink, grid, s));
+                                    ch->dev, 0, nch, fa, sink, grid, s, tail));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return COADAPT_OK;
 }
@@ -571,7 +582,8 @@ int stream_host_k1(coadapt_gns* g, const coadapt_plan* p, const void* host,
 // profiles/r01c_k1_tma.txt).  Returns false (nothing launched) when the
 // buckets do not qualify; *rc is the launch status otherwise.
 bool try_tma_k1(coadapt_gns* g, const coadapt_plan* p, const void* const* buckets,
-                int count, int slot0, cudaStream_t s, int* rc) {
+                int count, int slot0, cudaStream_t s, int* rc,
+                const coadapt::dev::Tail* tail = nullptr) {
   if (!use_tma_path() || count < 1 || count > coadapt::dev::kMaxFusedM) return false;
   for (int j = 0; j < count; ++j)
     if (!buckets[j] || (reinterpret_cast<uintptr_t>(buckets[j]) & 15)) return false;
@@ -583,8 +595,53 @@ bool try_tma_k1(coadapt_gns* g, const coadapt_plan* p, const void* const* bucket
   }
   fa.slot0 = slot0;
   fa.gslot = -1;
-  *rc = launch_fused_tma_all(g, const_cast<coadapt_plan*>(p), fa, count, s);
+  *rc = launch_fused_tma_all(g, const_cast<coadapt_plan*>(p), fa, count, s, tail);
   return true;
+}
+
+// The step's finalize carried by its last reduction (coadapt_gns_*_finalize):
+// mode 2 exchanges the slots over the attached NVLink mailboxes first.
+int make_tail(coadapt_gns* g, int64_t tokens, coadapt::dev::Tail* t) {
+  if (tokens < 0) return fail(COADAPT_E_VALIDATION, "tokens must be >= 0");
+  std::memset(t, 0, sizeof(*t));
+  t->p2p.fin = coadapt::dev::FinalizeArgs{g->slots, g->N, g->global_batch, tokens,
+                                          g->state, g->result};
+  t->p2p.slots = g->slots;
+  if (g->mbox_rank >= 0 && g->mbox_world > 1) {
+    if (g->N + 1 > g->mbox_cap)
+      return fail(COADAPT_E_VALIDATION,
+                  "d*M grew past the mailbox capacity: recreate the mailboxes");
+    t->mode = 2;
+    t->p2p.world = g->mbox_world;
+    t->p2p.rank = g->mbox_rank;
+    t->p2p.cap = g->mbox_cap;
+    t->p2p.timeout_ns = 10'000'000'000ll;
+    for (int q = 0; q < g->mbox_world; ++q) t->p2p.mbox[q] = g->mbox_peers[q];
+    return COADAPT_OK;
+  }
+  if (g->comm && g->nranks > 1)
+    return fail(COADAPT_E_VALIDATION,
+                "in-pass finalize across ranks needs the NVLink mailboxes "
+                "(coadapt_gns_attach_mailboxes); with NCCL use allreduce + finalize");
+  t->mode = 1;
+  return COADAPT_OK;
+}
+
+// result D2H + completion event, as after coadapt_gns_finalize
+int finish_result(coadapt_gns* g, cudaStream_t s) {
+  CU(cudaMemcpyAsync(g->result_host, g->result, sizeof(coadapt_gns_result),
+                     cudaMemcpyDeviceToHost, s));
+  // Under stream capture a plain record only orders nodes inside the graph;
+  // an external record node makes every replay signal result_ready, so
+  // read_result() after graph.replay() waits for that replay's D2H.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(s, &cap));
+  if (cap == cudaStreamCaptureStatusActive)
+    CU(cudaEventRecordWithFlags(g->result_ready, s, cudaEventRecordExternal));
+  else
+    CU(cudaEventRecord(g->result_ready, s));
+  g->finalized = true;
+  return COADAPT_OK;
 }
 
 }  // namespace
@@ -799,9 +856,53 @@ int coadapt_gns_micro_sqnorm_batched(coadapt_gns* g, const coadapt_plan* p,
   return COADAPT_OK;
 }
 
+namespace {
+int fused_impl(coadapt_gns* g, const coadapt_plan* p, const void* const* buckets,
+               int micro_count, void* stream, const coadapt::dev::Tail* tail);
+int mean_impl(coadapt_gns* g, const coadapt_plan* p, const void* mean_grad,
+              void* stream, const coadapt::dev::Tail* tail);
+}  // namespace
+
 int coadapt_gns_fused_sqnorm(coadapt_gns* g, const coadapt_plan* p,
                              const void* const* buckets, int micro_count,
                              void* stream) {
+  return fused_impl(g, p, buckets, micro_count, stream, nullptr);
+}
+
+int coadapt_gns_fused_sqnorm_finalize(coadapt_gns* g, const coadapt_plan* p,
+                                      const void* const* buckets,
+                                      int micro_count, int64_t tokens,
+                                      void* stream) {
+  if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
+  coadapt::dev::Tail t;
+  if (int rc = make_tail(g, tokens, &t)) return rc;
+  if (int rc = fused_impl(g, p, buckets, micro_count, stream, &t)) return rc;
+  GUARD(g->device);
+  return finish_result(g, static_cast<cudaStream_t>(stream));
+}
+
+int coadapt_gns_mean_sqnorm(coadapt_gns* g, const coadapt_plan* p,
+                            const void* mean_grad, void* stream) {
+  return mean_impl(g, p, mean_grad, stream, nullptr);
+}
+
+int coadapt_gns_mean_sqnorm_finalize(coadapt_gns* g, const coadapt_plan* p,
+                                     const void* mean_grad, int64_t tokens,
+                                     void* stream) {
+  if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
+  coadapt::dev::Tail t;
+  if (int rc = make_tail(g, tokens, &t)) return rc;
+  if (int rc = mean_impl(g, p, mean_grad, stream, &t)) return rc;
+  GUARD(g->device);
+  return finish_result(g, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+namespace {
+
+int fused_impl(coadapt_gns* g, const coadapt_plan* p, const void* const* buckets,
+               int micro_count, void* stream, const coadapt::dev::Tail* tail) {
   if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
   if (p->device != g->device)
     return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
@@ -834,13 +935,16 @@ int coadapt_gns_fused_sqnorm(coadapt_gns* g, const coadapt_plan* p,
   // the LDG form of the same pass
   if (use_tma_path() && mod0 == 0)
     return launch_fused_tma_all(g, const_cast<coadapt_plan*>(p), fa,
-                                micro_count, static_cast<cudaStream_t>(stream));
-  return launch_fused_window(g, p, fa, micro_count, Window{0, p->active},
-                             static_cast<cudaStream_t>(stream));
+                                micro_count, static_cast<cudaStream_t>(stream), tail);
+  if (int rc = launch_fused_window(g, p, fa, micro_count, Window{0, p->active},
+                                   static_cast<cudaStream_t>(stream)))
+    return rc;
+  return tail ? launch_tail_separately(*tail, static_cast<cudaStream_t>(stream))
+              : COADAPT_OK;
 }
 
-int coadapt_gns_mean_sqnorm(coadapt_gns* g, const coadapt_plan* p,
-                            const void* mean_grad, void* stream) {
+int mean_impl(coadapt_gns* g, const coadapt_plan* p, const void* mean_grad,
+              void* stream, const coadapt::dev::Tail* tail) {
   if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
   if (p->device != g->device)
     return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
@@ -850,7 +954,8 @@ int coadapt_gns_mean_sqnorm(coadapt_gns* g, const coadapt_plan* p,
   GUARD(g->device);
   {
     int rc = -1;
-    if (try_tma_k1(g, p, &mean_grad, 1, g->N, static_cast<cudaStream_t>(stream), &rc))
+    if (try_tma_k1(g, p, &mean_grad, 1, g->N, static_cast<cudaStream_t>(stream), &rc,
+                   tail))
       return rc;
   }
   BatchArgs jobs;
@@ -858,9 +963,16 @@ int coadapt_gns_mean_sqnorm(coadapt_gns* g, const coadapt_plan* p,
   jobs.count = 1;
   jobs.ptr[0] = mean_grad;
   jobs.slot[0] = g->N;
-  return launch_batch(g, p, jobs, Window{0, p->active},
-                      static_cast<cudaStream_t>(stream));
+  if (int rc = launch_batch(g, p, jobs, Window{0, p->active},
+                            static_cast<cudaStream_t>(stream)))
+    return rc;
+  return tail ? launch_tail_separately(*tail, static_cast<cudaStream_t>(stream))
+              : COADAPT_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
                                   const void* const* host_buckets,
@@ -1278,16 +1390,7 @@ int coadapt_gns_allreduce_finalize_p2p(coadapt_gns* g, int64_t tokens,
   for (int q = 0; q < a.world; ++q) a.mbox[q] = g->mbox_peers[q];
   CU(coadapt::dev::launch_p2p_finalize(a, s));
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  CU(cudaMemcpyAsync(g->result_host, g->result, sizeof(coadapt_gns_result),
-                     cudaMemcpyDeviceToHost, s));
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  CU(cudaStreamIsCapturing(s, &cap));
-  if (cap == cudaStreamCaptureStatusActive)
-    CU(cudaEventRecordWithFlags(g->result_ready, s, cudaEventRecordExternal));
-  else
-    CU(cudaEventRecord(g->result_ready, s));
-  g->finalized = true;
-  return COADAPT_OK;
+  return finish_result(g, s);
 }
 
 int coadapt_gns_finalize(coadapt_gns* g, int64_t tokens, void* stream) {
@@ -1299,19 +1402,7 @@ int coadapt_gns_finalize(coadapt_gns* g, int64_t tokens, void* stream) {
                                g->state, g->result};
   CU(coadapt::dev::launch_finalize(a, s));
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  CU(cudaMemcpyAsync(g->result_host, g->result, sizeof(coadapt_gns_result),
-                     cudaMemcpyDeviceToHost, s));
-  // Under stream capture a plain record only orders nodes inside the graph;
-  // an external record node makes every replay signal result_ready, so
-  // read_result() after graph.replay() waits for that replay's D2H.
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  CU(cudaStreamIsCapturing(s, &cap));
-  if (cap == cudaStreamCaptureStatusActive)
-    CU(cudaEventRecordWithFlags(g->result_ready, s, cudaEventRecordExternal));
-  else
-    CU(cudaEventRecord(g->result_ready, s));
-  g->finalized = true;
-  return COADAPT_OK;
+  return finish_result(g, s);
 }
 
 int coadapt_gns_read_result(coadapt_gns* g, coadapt_gns_result* out) {

@@ -128,6 +128,21 @@ void GnsDevicePlan::record_mean_gradient(const BucketLayout& layout,
   check(coadapt_gns_mean_sqnorm(g_, layout.handle(), mean, stream));
 }
 
+void GnsDevicePlan::record_fused_finalize(const BucketLayout& layout,
+                                          std::span<const void* const> buckets,
+                                          std::int64_t tokens, void* stream) {
+  check(coadapt_gns_fused_sqnorm_finalize(g_, layout.handle(), buckets.data(),
+                                          (int)buckets.size(), tokens, stream));
+}
+
+void GnsDevicePlan::record_mean_gradient_finalize(const BucketLayout& layout,
+                                                  const void* mean,
+                                                  std::int64_t tokens,
+                                                  void* stream) {
+  check(coadapt_gns_mean_sqnorm_finalize(g_, layout.handle(), mean, tokens,
+                                         stream));
+}
+
 void GnsDevicePlan::record_micro_bucket_host(const BucketLayout& layout,
                                              const void* bucket, int dp_index,
                                              int micro, void* stream) {

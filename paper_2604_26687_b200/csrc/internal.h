@@ -60,10 +60,11 @@ cudaError_t launch_fused(int dtype, int M, const Range* ranges, int nranges,
 // range: range k owns chunks [prefix[k], prefix[k+1]) covering its
 // intersections with the absolute windows [j*P, (j+1)*P).
 int tma_chunk_elems(int dtype, int M, bool mean = true);  // P
+struct Tail;
 cudaError_t launch_fused_tma(int dtype, int M, const Range* ranges, int nranges,
                              const uint64_t* prefix, uint64_t c_begin,
                              uint64_t c_end, const FusedArgs& args, Sink sink,
-                             int grid, cudaStream_t s);
+                             int grid, cudaStream_t s, const Tail* tail = nullptr);
 // max resident CTAs per SM for the kernel that launch_* would pick
 int occupancy_sqnorm(int dtype);
 int occupancy_fused(int dtype, int M);
@@ -125,6 +126,17 @@ struct P2PArgs {
   char* mbox[kMaxPeers];     // rank q's mailbox (peer-mapped; own = local)
 };
 cudaError_t launch_p2p_finalize(const P2PArgs& a, cudaStream_t s);
+
+// Finalize carried by the step's last reduction launch (north_star item 2:
+// the estimators "fused into the same pass"): after the last CTA has
+// combined the partials into the slots it runs K3 (mode 1), or first
+// exchanges the slots over the NVLink mailboxes like p2p_finalize_kernel
+// (mode 2).  mode 0: no tail.
+struct Tail {
+  int32_t mode;
+  int32_t reserved_;
+  P2PArgs p2p;  // mode 1 uses p2p.fin only
+};
 inline size_t mailbox_bytes(int world, int cap) {
   return (size_t)2 * world * cap * sizeof(double) + (size_t)2 * world * 8 + 8;
 }

@@ -29,6 +29,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <cstring>
+
 #include "../../include/coadapt_cuda.h"
 #include "internal.h"
 
@@ -251,7 +253,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // partials[o * G + cta]; the CTA that takes the last ticket sums each
 // output's G partials in a fixed order and adds scale*sum into slots[slot].
 template <int NT>
-__device__ __forceinline__ void last_cta_combine(const Sink& sink, int nout,
+__device__ __forceinline__ bool last_cta_combine(const Sink& sink, int nout,
                                                  const int32_t* out_slot,
                                                  const double* out_scale,
                                                  double* red) {
@@ -264,7 +266,7 @@ __device__ __forceinline__ void last_cta_combine(const Sink& sink, int nout,
     is_last = (t == (unsigned)G - 1u);
   }
   __syncthreads();
-  if (!is_last) return;
+  if (!is_last) return false;
   __threadfence();
   for (int o = 0; o < nout; ++o) {
     double v = 0.0;
@@ -278,7 +280,12 @@ __device__ __forceinline__ void last_cta_combine(const Sink& sink, int nout,
     }
   }
   if (threadIdx.x == 0) *sink.ticket = 0u;  // ready for the next launch
+  return true;
 }
+
+// defined with K3 / X1 below; the TMA kernel's last CTA may run them
+__device__ void finalize_body(const FinalizeArgs& a);
+__device__ void p2p_exchange_finalize(const P2PArgs& a);
 
 // This CTA's equal share of the window [e_begin, e_end) of active elements,
 // rounded to 64-element multiples so bodies stay 16B-aligned.
@@ -682,7 +689,8 @@ template <int DT, int M, int V, bool MEAN>
 __global__ void __launch_bounds__(TmaCfg<DT, M, V>::NT, 1)
     fused_tma_kernel(const Range* __restrict__ R, int nr,
                      const uint64_t* __restrict__ prefix, uint64_t c_begin,
-                     uint64_t c_end, const FusedArgs args, Sink sink) {
+                     uint64_t c_end, const FusedArgs args, Sink sink,
+                     const __grid_constant__ Tail tail) {
   // Two consumer groups of NW/2 warps take alternate chunks; every thread
   // owns whole positions of a chunk (tma_consume_cols), so per-thread state
   // is M fp64 accumulators and nothing is read twice from shared memory.
@@ -770,7 +778,16 @@ __global__ void __launch_bounds__(TmaCfg<DT, M, V>::NT, 1)
         threadIdx.x < M ? args.slot0 + (int)threadIdx.x : args.gslot;
     out_scale[threadIdx.x] = threadIdx.x < M ? 1.0 : args.gscale;
   }
-  last_cta_combine<C::NT>(sink, MEAN ? M + 1 : M, out_slot, out_scale, red);
+  const bool last =
+      last_cta_combine<C::NT>(sink, MEAN ? M + 1 : M, out_slot, out_scale, red);
+  if (tail.mode == 0 || !last) return;
+  // the step's last reduction: this CTA holds the final slots (its own
+  // thread 0 wrote them; earlier launches are stream-ordered before it)
+  __syncthreads();
+  if (tail.mode == 2)
+    p2p_exchange_finalize(tail.p2p);
+  else if (threadIdx.x == 0)
+    finalize_body(tail.p2p.fin);
 }
 
 // ---------------------------------------------------------------- KA
@@ -1222,7 +1239,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 // current epoch before it can finish and start the next), so the block it
 // overwrites next was read already.  A peer that never arrives turns into a
 // status-2 result after timeout_ns instead of a hang.
-__global__ void __launch_bounds__(256) p2p_finalize_kernel(const __grid_constant__ P2PArgs a) {
+__device__ void p2p_exchange_finalize(const P2PArgs& a) {
   const int nv = a.fin.n + 1, tid = threadIdx.x;
   const size_t data_doubles = (size_t)2 * a.world * a.cap;
   // the step counter lives in device memory after this rank's flags: every
@@ -1288,6 +1305,10 @@ __global__ void __launch_bounds__(256) p2p_finalize_kernel(const __grid_constant
   }
   __syncthreads();
   if (tid == 0) finalize_body(a.fin);
+}
+
+__global__ void __launch_bounds__(256) p2p_finalize_kernel(const __grid_constant__ P2PArgs a) {
+  p2p_exchange_finalize(a);
 }
 
 // ---------------------------------------------------------------- K0
@@ -1542,11 +1563,15 @@ int tma_chunk_elems(int dtype, int M, bool mean) { return tma_kernel(dtype, M, m
 cudaError_t launch_fused_tma(int dtype, int M, const Range* ranges, int nranges,
                              const uint64_t* prefix, uint64_t c_begin,
                              uint64_t c_end, const FusedArgs& fa, Sink sink,
-                             int grid, cudaStream_t s) {
+                             int grid, cudaStream_t s, const Tail* tail) {
   const TmaFn f = tma_kernel(dtype, M, fa.gslot >= 0);
   if (!f.fn) return cudaErrorInvalidValue;
+  Tail none;
+  std::memset(&none, 0, sizeof(none));
+  const Tail& t = tail ? *tail : none;
   void* args[] = {(void*)&ranges, (void*)&nranges, (void*)&prefix,
-                  (void*)&c_begin, (void*)&c_end, (void*)&fa, (void*)&sink};
+                  (void*)&c_begin, (void*)&c_end, (void*)&fa, (void*)&sink,
+                  (void*)&t};
   return cudaLaunchKernel(f.fn, dim3(grid), dim3(f.nt), args, f.smem, s);
 }
 

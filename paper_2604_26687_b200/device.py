@@ -170,6 +170,22 @@ class GnsDevice:
         ptrs = (C.c_void_p * max(1, k))(*[_bucket(plan, b) for b in buckets])
         check(lib().coadapt_gns_fused_sqnorm(self.handle, plan.handle, ptrs, k, _stream(stream)))
 
+    def fused_sqnorm_finalize(self, plan: BucketPlan, buckets: Sequence, tokens_this_step: int,
+                              stream=None) -> None:
+        """The step's last fused pass with finalize (and, with mailboxes
+        attached, the NVLink slot exchange) in its last CTA."""
+        k = len(buckets)
+        ptrs = (C.c_void_p * max(1, k))(*[_bucket(plan, b) for b in buckets])
+        check(lib().coadapt_gns_fused_sqnorm_finalize(self.handle, plan.handle, ptrs, k,
+                                                      int(tokens_this_step), _stream(stream)))
+
+    def mean_sqnorm_finalize(self, plan: BucketPlan, mean_grad, tokens_this_step: int,
+                             stream=None) -> None:
+        """d > 1: the step's last mean-slice read with finalize in the pass."""
+        check(lib().coadapt_gns_mean_sqnorm_finalize(self.handle, plan.handle,
+                                                     _bucket(plan, mean_grad, "mean_grad"),
+                                                     int(tokens_this_step), _stream(stream)))
+
     def fused_sqnorm_host(self, plan: BucketPlan, host_buckets: Sequence, stream=None) -> None:
         k = len(host_buckets)
         ptrs = (C.c_void_p * max(1, k))(*[_bucket(plan, b, "host bucket", host=True)

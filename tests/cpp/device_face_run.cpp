@@ -157,6 +157,22 @@ int main(int argc, char** argv) {
           std::printf(", ");
         }
       }
+      // the finalize in the same pass (record_fused_finalize) == the
+      // separate record_fused + finalize, bit for bit
+      {
+        GnsDevicePlan sep(1, M, M * Bm, 0), inp(1, M, M * Bm, 0);
+        sep.begin_step(stream);
+        sep.record_fused(layout, ptrs, stream);
+        sep.finalize((std::int64_t)M * Bm * 2048, stream);
+        inp.begin_step(stream);
+        inp.record_fused_finalize(layout, ptrs, (std::int64_t)M * Bm * 2048, stream);
+        const DeviceStepResult a = sep.result(), b = inp.result();
+        if (!same(a.stats.signal, b.stats.signal) || !same(a.stats.noise, b.stats.noise) ||
+            !same(a.b_simple, b.b_simple) || !same(a.state.ema_signal, b.state.ema_signal)) {
+          std::fprintf(stderr, "record_fused_finalize differs from record_fused + finalize\n");
+          bad |= 1;
+        }
+      }
       // host buckets (pinned) through the same plan: record_fused_host
       std::vector<void*> host(M);
       for (int m = 0; m < M; ++m) {

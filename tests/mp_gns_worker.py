@@ -22,9 +22,12 @@ from paper_2604_26687_b200 import dist as Dist  # noqa: E402
 from paper_2604_26687_b200 import layout as Lay  # noqa: E402
 
 
-def run_job(g, lays, ranks, M, d, seed, unit, fused):
+def run_job(g, lays, ranks, M, d, seed, unit, fused, final_tokens=None):
+    """final_tokens: the rank's last reduction carries the finalize (and the
+    NVLink slot exchange) in its last CTA (coadapt_gns_*_finalize)."""
     g.begin_step()
-    for vr in ranks:
+    for k, vr in enumerate(ranks):
+        last = final_tokens is not None and k + 1 == len(ranks)
         lay = lays[vr]
         i_d = lay.coords[0]
         plan = D.BucketPlan(lay.segments, lay.numel, L.BF16, torch.cuda.current_device())
@@ -34,14 +37,20 @@ def run_job(g, lays, ranks, M, d, seed, unit, fused):
             D.synth_fill(b, lay.gen, seed, i_d * M + m, Lay.G0, unit)
             bufs.append(b)
         if fused:
-            g.fused_sqnorm(plan, bufs)
+            if last:
+                g.fused_sqnorm_finalize(plan, bufs, final_tokens)
+            else:
+                g.fused_sqnorm(plan, bufs)
         else:
             g.micro_sqnorm_batched(plan, bufs, [i_d] * M, list(range(M)))
             mean = torch.empty(lay.numel, dtype=torch.bfloat16, device="cuda")
             D.synth_mean_fill(mean, lay.gen, seed, 0, d * M, Lay.G0, unit)
             sl = D.BucketPlan(lay.segments, lay.numel, L.BF16, torch.cuda.current_device(),
                               slice_index=i_d, slice_count=d)
-            g.mean_sqnorm(sl, mean)
+            if last:
+                g.mean_sqnorm_finalize(sl, mean, final_tokens)
+            else:
+                g.mean_sqnorm(sl, mean)
 
 
 def graph_p2p_case(lays, mine, M, d, unit, local, world, rank):
@@ -157,6 +166,24 @@ def main():
         case["p2p_phi_identical_on_all_ranks"] = bool(lo2.item() == hi2.item())
         ok = ok and case["p2p_max_rel_slots_vs_nccl"] <= 1e-14 and \
             case["p2p_phi_identical_on_all_ranks"] and case["p2p_b_simple_rel"] <= 1e-12
+        # the slot exchange + finalize inside the last reduction's last CTA
+        g3 = D.GnsDevice(d, M, d * M, local)
+        bases3 = Dist.attach_p2p(g3, dist, world, rank)
+        run_job(g3, lays, mine, M, d, 0xC0905, unit, fused, final_tokens=d * M * 2048)
+        r3 = g3.result()
+        p3 = g3.partials()
+        case["inpass_max_rel_slots_vs_nccl"] = float(np.max(np.abs(p3 - parts) /
+                                                            np.maximum(np.abs(parts), 1e-300)))
+        case["inpass_b_simple_rel"] = abs(r3.b_simple - r.b_simple) / abs(r.b_simple)
+        case["inpass_bitwise_vs_p2p_kernel"] = bool(np.array_equal(p3, p2) and
+                                                    r3.b_simple == r2.b_simple)
+        ok = ok and r3.status == 0 and case["inpass_max_rel_slots_vs_nccl"] <= 1e-14 and \
+            case["inpass_bitwise_vs_p2p_kernel"]
+        torch.cuda.synchronize()
+        dist.barrier()
+        for b in bases3:
+            D.ipc_close(b)
+        g3.close()
         # tail latency: NCCL all-reduce + finalize vs the fused P2P kernel
         s = torch.cuda.current_stream()
         for name, fn in (("nccl", lambda: (g.allreduce(), g.finalize(1))),
