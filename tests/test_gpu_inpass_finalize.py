@@ -27,8 +27,9 @@ def _same(a, b):
     assert ra.state.as_tuple() == rb.state.as_tuple()
     assert (ra.stats.signal, ra.stats.noise, ra.stats.noise_raw, ra.stats.mean_grad_sq) == \
         (rb.stats.signal, rb.stats.noise, rb.stats.noise_raw, rb.stats.mean_grad_sq)
-    assert (ra.phi, ra.b_simple, ra.phi_available, ra.status) == \
-        (rb.phi, rb.b_simple, rb.phi_available, rb.status)
+    assert np.array_equal(np.array([ra.phi, ra.b_simple]), np.array([rb.phi, rb.b_simple]),
+                          equal_nan=True)  # phi is NaN while unavailable
+    assert (ra.phi_available, ra.status) == (rb.phi_available, rb.status)
     return ra
 
 
