@@ -192,7 +192,8 @@ void orc_score_candidates(const orc_entry* cands, size_t n, double phi,
 
 /* x = G_i + zeta_{n,i}, G_i = +-g0 (sign from hash(seed, gidx)), zeta =
  * float(IrwinHall4 integer) * noise_unit, rounded RNE to dtype.  Bit-exact
- * twin of the device generator (csrc/synth.cu). */
+ * twin of the device generator K0 (synth_kernel in
+ * paper_2604_26687_b200/csrc/kernels.cu). */
 void orc_synth_fill(void* dst, int dtype, const orc_gen_segment* segs,
                     size_t nseg, uint64_t seed, uint64_t sample, float g0,
                     float noise_unit);

@@ -669,6 +669,7 @@ int coadapt_device_info(int device, int* sm, int* l2, int* major, int* minor) {
 int coadapt_plan_create(const coadapt_segment* segs, size_t nseg,
                         uint64_t bucket_numel, int dtype, int device,
                         coadapt_plan** out) {
+  COADAPT_NVTX("coadapt_plan_create");
   return plan_make(segs, nseg, bucket_numel, dtype, device, 0, bucket_numel,
                    out);
 }
@@ -676,6 +677,7 @@ int coadapt_plan_create(const coadapt_segment* segs, size_t nseg,
 int coadapt_plan_create_slice(const coadapt_segment* segs, size_t nseg,
                               uint64_t bucket_numel, int dtype, int device,
                               int index, int count, coadapt_plan** out) {
+  COADAPT_NVTX("coadapt_plan_create_slice");
   if (count < 1 || index < 0 || index >= count)
     return fail(COADAPT_E_VALIDATION, "slice index/count out of range");
   auto cut = [&](int i) -> uint64_t {
@@ -800,6 +802,7 @@ int coadapt_gns_reshape(coadapt_gns* g, int dp_size, int micro_count,
 }
 
 int coadapt_gns_begin_step(coadapt_gns* g, void* stream) {
+  COADAPT_NVTX("coadapt_gns_begin_step");
   if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
   GUARD(g->device);
   CU(cudaMemsetAsync(g->slots, 0, sizeof(double) * (g->N + 1),
@@ -819,6 +822,7 @@ int coadapt_gns_micro_sqnorm_batched(coadapt_gns* g, const coadapt_plan* p,
                                      const int32_t* dp_index,
                                      const int32_t* micro, int count,
                                      void* stream) {
+  COADAPT_NVTX("coadapt_gns_micro_sqnorm_batched");
   if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
   if (p->device != g->device)
     return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
@@ -866,6 +870,7 @@ int mean_impl(coadapt_gns* g, const coadapt_plan* p, const void* mean_grad,
 int coadapt_gns_fused_sqnorm(coadapt_gns* g, const coadapt_plan* p,
                              const void* const* buckets, int micro_count,
                              void* stream) {
+  COADAPT_NVTX("coadapt_gns_fused_sqnorm");
   return fused_impl(g, p, buckets, micro_count, stream, nullptr);
 }
 
@@ -873,6 +878,7 @@ int coadapt_gns_fused_sqnorm_finalize(coadapt_gns* g, const coadapt_plan* p,
                                       const void* const* buckets,
                                       int micro_count, int64_t tokens,
                                       void* stream) {
+  COADAPT_NVTX("coadapt_gns_fused_sqnorm_finalize");
   if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
   coadapt::dev::Tail t;
   if (int rc = make_tail(g, tokens, &t)) return rc;
@@ -883,12 +889,14 @@ int coadapt_gns_fused_sqnorm_finalize(coadapt_gns* g, const coadapt_plan* p,
 
 int coadapt_gns_mean_sqnorm(coadapt_gns* g, const coadapt_plan* p,
                             const void* mean_grad, void* stream) {
+  COADAPT_NVTX("coadapt_gns_mean_sqnorm");
   return mean_impl(g, p, mean_grad, stream, nullptr);
 }
 
 int coadapt_gns_mean_sqnorm_finalize(coadapt_gns* g, const coadapt_plan* p,
                                      const void* mean_grad, int64_t tokens,
                                      void* stream) {
+  COADAPT_NVTX("coadapt_gns_mean_sqnorm_finalize");
   if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
   coadapt::dev::Tail t;
   if (int rc = make_tail(g, tokens, &t)) return rc;
@@ -977,6 +985,7 @@ extern "C" {
 int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
                                   const void* const* host_buckets,
                                   int micro_count, void* stream) {
+  COADAPT_NVTX("coadapt_gns_fused_sqnorm_host");
   if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
   if (p->device != g->device)
     return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
@@ -1046,6 +1055,7 @@ int coadapt_gns_fused_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
 int coadapt_gns_micro_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
                                   const void* host_bucket, int dp_index,
                                   int micro, void* stream) {
+  COADAPT_NVTX("coadapt_gns_micro_sqnorm_host");
   if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
   if (p->device != g->device)
     return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
@@ -1061,6 +1071,7 @@ int coadapt_gns_micro_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
 
 int coadapt_gns_mean_sqnorm_host(coadapt_gns* g, const coadapt_plan* p,
                                  const void* host_mean, void* stream) {
+  COADAPT_NVTX("coadapt_gns_mean_sqnorm_host");
   if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
   if (p->device != g->device)
     return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
@@ -1076,6 +1087,7 @@ int coadapt_gns_accumulate(coadapt_gns* g, const coadapt_plan* p,
                            float* main_grad, const void* micro_grad,
                            int dp_index, int micro, int flags,
                            double mean_scale_sq, void* stream) {
+  COADAPT_NVTX("coadapt_gns_accumulate");
   if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
   if (p->device != g->device)
     return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
@@ -1162,6 +1174,7 @@ int coadapt_ipc_close(void* dev_ptr) {
 }
 
 int coadapt_gns_barrier(coadapt_gns* g, void* stream) {
+  COADAPT_NVTX("coadapt_gns_barrier");
   if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
   if (!g->comm || g->nranks == 1) return COADAPT_OK;
   GUARD(g->device);
@@ -1231,12 +1244,14 @@ int coadapt_gns_reduce_scatter_sqnorm(coadapt_gns* g, const coadapt_plan* p,
                                       const void* const* replicas, int d,
                                       int dp_rank, void* out_slice,
                                       double scale, void* stream) {
+  COADAPT_NVTX("coadapt_gns_reduce_scatter_sqnorm");
   return rs_common(g, p, replicas, d, dp_rank, out_slice, false, scale, stream);
 }
 
 int coadapt_gns_allreduce_sqnorm(coadapt_gns* g, const coadapt_plan* p,
                                  void* const* replicas, int d, int dp_rank,
                                  double scale, void* stream) {
+  COADAPT_NVTX("coadapt_gns_allreduce_sqnorm");
   return rs_common(g, p, const_cast<const void* const*>(replicas), d, dp_rank,
                    nullptr, true, scale, stream);
 }
@@ -1293,6 +1308,7 @@ int coadapt_gns_attach_nccl_all(coadapt_gns* const* gs, int n) {
 
 int coadapt_gns_allreduce_group(coadapt_gns* const* gs, void* const* streams,
                                 int n) {
+  COADAPT_NVTX("coadapt_gns_allreduce_group");
   if (!gs || !streams || n < 1)
     return fail(COADAPT_E_VALIDATION, "need n >= 1 gns handles and streams");
   for (int i = 0; i < n; ++i) {
@@ -1318,6 +1334,7 @@ int coadapt_gns_allreduce_group(coadapt_gns* const* gs, void* const* streams,
 }
 
 int coadapt_gns_allreduce(coadapt_gns* g, void* stream) {
+  COADAPT_NVTX("coadapt_gns_allreduce");
   if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
   if (!g->comm || g->nranks == 1) return COADAPT_OK;  // local sum only
   GUARD(g->device);
@@ -1369,6 +1386,7 @@ int coadapt_gns_attach_mailboxes(coadapt_gns* g, int nranks, int rank,
 
 int coadapt_gns_allreduce_finalize_p2p(coadapt_gns* g, int64_t tokens,
                                        void* stream) {
+  COADAPT_NVTX("coadapt_gns_allreduce_finalize_p2p");
   if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
   if (tokens < 0) return fail(COADAPT_E_VALIDATION, "tokens must be >= 0");
   if (g->mbox_rank < 0)
@@ -1394,6 +1412,7 @@ int coadapt_gns_allreduce_finalize_p2p(coadapt_gns* g, int64_t tokens,
 }
 
 int coadapt_gns_finalize(coadapt_gns* g, int64_t tokens, void* stream) {
+  COADAPT_NVTX("coadapt_gns_finalize");
   if (!g) return fail(COADAPT_E_VALIDATION, "gns is NULL");
   if (tokens < 0) return fail(COADAPT_E_VALIDATION, "tokens must be >= 0");
   GUARD(g->device);
@@ -1456,6 +1475,7 @@ int coadapt_gns_set_state(coadapt_gns* g, const coadapt_gns_state* in) {
 
 int coadapt_sqnorm_device(const void* v, uint64_t n, int dtype, int device,
                           double* out, void* stream) {
+  COADAPT_NVTX("coadapt_sqnorm_device");
   if (!out) return fail(COADAPT_E_VALIDATION, "out is NULL");
   if (int rc = validate_dtype(dtype, true)) return rc;
   std::lock_guard<std::mutex> lock(g_oneshot_mu);
@@ -1502,6 +1522,7 @@ int coadapt_sqnorm_device(const void* v, uint64_t n, int dtype, int device,
 
 int coadapt_sqnorm_host(const void* v, uint64_t n, int dtype, int device,
                         double* out) {
+  COADAPT_NVTX("coadapt_sqnorm_host");
   if (!out) return fail(COADAPT_E_VALIDATION, "out is NULL");
   if (int rc = validate_dtype(dtype, true)) return rc;
   if (n == 0) {

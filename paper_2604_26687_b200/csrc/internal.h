@@ -3,10 +3,22 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 namespace coadapt {
 namespace dev {
+
+// NVTX range over one C-ABI call (host side: the launches it enqueues show
+// under the call's name in Nsight Systems / ncu --nvtx).  Header-only NVTX3:
+// a no-op unless a tool is attached.
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
+#define COADAPT_NVTX(name) ::coadapt::dev::NvtxScope coadapt_nvtx_scope_(name)
 
 // One maximal run of same-weight, non-zero-weight bucket elements.
 // cum_begin is its first index in the "active" (compacted) element space.

@@ -45,6 +45,7 @@
 #include <thread>
 
 #include "../../include/coadapt_cuda.h"
+#include "internal.h"
 
 namespace coadapt_capi {
 void set_error(const char* msg);
@@ -481,6 +482,7 @@ uint64_t coadapt_nvls_bytes(const coadapt_nvls* o) { return o ? o->bytes : 0; }
 
 int coadapt_nvls_allreduce(coadapt_nvls* o, int dtype, uint64_t numel, int dp_rank,
                            double scale, void* stream) {
+  COADAPT_NVTX("coadapt_nvls_allreduce");
   if (!o || !o->bound) return fail(COADAPT_E_VALIDATION, "object not bound");
   // fp32 only: the switch's bf16 reduction rounds differently from RNE and
   // the difference is one-sided (measured: ~20 % of elements 1 ulp off,

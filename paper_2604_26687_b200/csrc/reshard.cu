@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../../include/coadapt_cuda.h"
+#include "internal.h"
 #include "../../include/coadapt_reshard.h"
 #include "coadapt/errors.hpp"
 #include "coadapt/reshard.hpp"
@@ -383,6 +384,7 @@ int coadapt_reshard_execute(coadapt_reshard_plan* p, int role, int rank,
                             const void* const* src_packs, size_t n_src,
                             void* const* dst_packs, size_t n_dst,
                             int elem_bytes, int device, void* stream) {
+  COADAPT_NVTX("coadapt_reshard_execute");
   if (!p || !src_packs || !dst_packs)
     return fail(COADAPT_E_VALIDATION, "reshard: NULL argument");
   if (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4 && elem_bytes != 8)
