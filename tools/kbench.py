@@ -61,6 +61,8 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--kernels", default="k1,probe,k1f,accum",
                     help="comma list of k1, probe, k1f, accum")
+    ap.add_argument("--phi", type=float, default=256.0,
+                    help="synthetic noise scale of the data (power depends on the bits)")
     ap.add_argument("--sustain", type=float, default=0.0,
                     help="seconds of back-to-back launches per kernel (power-cap steady state)")
     args = ap.parse_args()
@@ -72,7 +74,9 @@ def main():
     es = D.ESIZE[dt]
     n = int(args.gb * 1e9 / es)
     x = torch.empty(n, dtype=tdt, device="cuda")
-    D.synth_fill(x, [(0, n, 0, n, n)], 1, 0, 2.0 ** -10, 1e-7)
+    from paper_2604_26687_b200 import layout as Lay
+    unit = Lay.noise_unit_for(args.phi, 1)
+    D.synth_fill(x, [(0, n, 0, n, n)], 1, 0, 2.0 ** -10, unit)
     plan = D.BucketPlan([(0, n, 1.0)], n, dt, 0)
     g = D.GnsDevice(1, args.fused_m, args.fused_m, 0)
     out = {"variant": os.environ.get("COADAPT_BF16_VARIANT", "default"), "dtype": args.dtype}
@@ -92,7 +96,7 @@ def main():
         nb = int(args.fused_gb * 1e9 / es / M)
         bufs = [torch.empty(nb, dtype=tdt, device="cuda") for _ in range(M)]
         for m, b in enumerate(bufs):
-            D.synth_fill(b, [(0, nb, 0, nb, nb)], 1, m, 2.0 ** -10, 1e-7)
+            D.synth_fill(b, [(0, nb, 0, nb, nb)], 1, m, 2.0 ** -10, unit)
         fplan = D.BucketPlan([(0, nb, 1.0)], nb, dt, 0)
         if "k1f" in ks:
             sec = timed(lambda: g.fused_sqnorm(fplan, bufs, s), args.reps, s)
