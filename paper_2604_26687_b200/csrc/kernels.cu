@@ -187,6 +187,22 @@ __device__ __forceinline__ double bf16_hi_s(uint32_t w) {
   return __hiloint2double(((w >> 3) & 0x0FFFE000u) + kExp485, 0);
 }
 
+// fp32 -> fp64 pair for an exact square without the XU: the fp32 bits moved
+// into fp64 position read as s * 2^-896 (zero and subnormals included), and
+// with 1792 added to the exponent field as s * 2^896 (every normal s); the
+// low 3 mantissa bits land in the low word, shared by both.  a * c == s * s
+// exactly (24 x 24 bits), so DFMA(a, c, g) == DFMA(s, s, g) bit for bit;
+// only an fp32-subnormal s (|s| < 2^-126) is off, by < 2^-251 absolute.
+#ifndef COADAPT_GSQ
+#define COADAPT_GSQ 0  // 1: measured 1.3 % slower sustained (profiles/r02_vacc_variants.txt)
+#endif
+__device__ __forceinline__ void f32_ac(float s, double& a, double& c) {
+  const uint32_t b = __float_as_uint(s);
+  const uint32_t hi = (b >> 3) & 0x0FFFFFFFu, lo = b << 29;
+  a = __hiloint2double(hi, lo);
+  c = __hiloint2double(hi | 0x70000000u, lo);
+}
+
 // acc += sum of squares of one vector, every square exact in fp64.
 // Each value goes to fp64 with one F2F on the XU pipe (bf16 straight from
 // the half-word), which with the 1 kW power cap is what bounds these
@@ -745,8 +761,14 @@ __device__ __forceinline__ void tma_consume_cols(const char* stage,
       double g = 0.0;
 #pragma unroll
       for (int e = 0; e < C::PV; ++e) {
+#if COADAPT_GSQ
+        double a, c;
+        f32_ac(sum[e], a, c);
+        g = fma(a, c, g);
+#else
         const double sd = sum[e];
         g = fma(sd, sd, g);
+#endif
       }
       gacc = WEIGHTED ? fma(w, g, gacc) : gacc + g;
     }
