@@ -179,13 +179,17 @@ void orc_fused_sqnorms(const void* const* bufs, int M, int dtype,
     double* pk = part + (size_t)k * (M + 1);
     for (int m = 0; m < M; ++m)
       pk[m] = range_sumsq_lanes(bufs[m], dtype, items[k].begin, items[k].end);
-    double acc = 0.0;
+    /* 8 fp64 lanes (lane j takes i = j mod 8) combined in lane order, the
+     * same fixed association as range_sumsq_lanes */
+    double lane[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (uint64_t i = items[k].begin; i < items[k].end; ++i) {
       float sum = 0.0f; /* Megatron main_grad: fp32, micro-batches in order */
       for (int m = 0; m < M; ++m) sum = sum + load_elem_f(bufs[m], dtype, i);
       const double sd = (double)sum;
-      acc += sd * sd;
+      lane[i & 7] += sd * sd;
     }
+    double acc = 0.0;
+    for (int j = 0; j < 8; ++j) acc += lane[j];
     for (int m = 0; m < M; ++m) pk[m] *= items[k].weight;
     pk[M] = items[k].weight * acc;
   }
