@@ -249,3 +249,23 @@ def test_trainer_main_grad_in_nvls_memory():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     rep = json.loads(lines[-1])
     assert rep["ok"], rep
+
+
+@pytest.mark.gpu
+def test_eight_rank_exchange_on_fewer_gpus():
+    """The 8-peer mailbox exchange (the 8 x B200 case gpurun cannot provide)
+    with 8 processes on the box's 2 or 4 GPUs: in-pass and standalone forms
+    equal the one-GPU job for 4 steps, phi bit-identical on all 8 ranks."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs (gpurun --gpus 2)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port", str(29300 + os.getpid() % 90),
+           os.path.join(HERE, "mp_p2p8_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    rep = json.loads(lines[-1])
+    print(json.dumps(rep))
+    assert rep["ok"], rep
