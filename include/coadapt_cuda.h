@@ -298,6 +298,22 @@ int coadapt_nvls_allreduce(coadapt_nvls* o, int dtype, uint64_t numel, int dp_ra
                            double scale, void* stream);
 int coadapt_nvls_destroy(coadapt_nvls* o);
 
+/* The fused DP gradient sync + mean-gradient norm through the switch (§8
+ * f2; Alg. 1 "standard gradient sync" + gbar^2): the DP
+ * group's fp32 buckets are one NVLS object (coadapt_nvls_bind, `multicast` =
+ * this rank's multicast view of the bucket start).  For this rank's slice of
+ * the plan (the coadapt_plan_create_slice cut, dp_rank of d) every load is
+ * one multimem.ld_reduce — the NVSwitch sums the d copies, so each GPU's
+ * links carry its slice once instead of (d-1)/d of the bucket — and the
+ * scaled result goes to out_slice (reduce-scatter, DistOpt) or, with
+ * out_slice == NULL, back through the multicast address into every GPU's
+ * copy (all-reduce, DDP); its weighted squared norm is added to slot N in
+ * the same pass.  Bracket with coadapt_gns_barrier like the P2P forms.
+ * fp32 only (the switch's bf16/fp16 rounding biases gbar^2). */
+int coadapt_gns_nvls_reduce_sqnorm(coadapt_gns* g, const coadapt_plan* p,
+                                   const void* multicast, int d, int dp_rank,
+                                   void* out_slice, double scale, void* stream);
+
 /* NCCL over NVLink: sum the N+1 slots over all ranks (Alg. 1 AllReduce,
  * PAPER.md:443; the reference models it as summation). */
 int coadapt_nccl_unique_id(void* out, size_t len); /* len >= 128 */

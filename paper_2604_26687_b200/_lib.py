@@ -236,6 +236,7 @@ SIGNATURES = {
     "coadapt_nvls_bytes": (U64, [P]),
     "coadapt_nvls_allreduce": (I, [P, I, U64, I, D, P]),
     "coadapt_nvls_destroy": (I, [P]),
+    "coadapt_gns_nvls_reduce_sqnorm": (I, [P, P, P, I, I, P, D, P]),
     # coadapt_host.h
     "coadapt_finalize_step": (I, [P, I64, I, D, I64, P]),
     "coadapt_finalize_step_vec": (I, [P, I64, I, P, U64, I64, P]),

@@ -1188,7 +1188,8 @@ int coadapt_gns_barrier(coadapt_gns* g, void* stream) {
 
 static int rs_common(coadapt_gns* g, const coadapt_plan* p,
                      const void* const* replicas, int d, int dp_rank,
-                     void* out_slice, bool inplace, double scale, void* stream) {
+                     void* out_slice, bool inplace, double scale, void* stream,
+                     const void* multicast = nullptr) {
   if (!g || !p) return fail(COADAPT_E_VALIDATION, "gns/plan is NULL");
   if (p->device != g->device)
     return fail(COADAPT_E_VALIDATION, "plan and gns live on different devices");
@@ -1198,18 +1199,28 @@ static int rs_common(coadapt_gns* g, const coadapt_plan* p,
     return fail(COADAPT_E_VALIDATION, "fp64 buckets are not supported here");
   if (d < 1 || d > coadapt::dev::kMaxReplicas || dp_rank < 0 || dp_rank >= d)
     return fail(COADAPT_E_VALIDATION, "need 1 <= d <= 8 and 0 <= dp_rank < d");
-  if (!replicas || (p->bucket_numel && !inplace && !out_slice))
+  if ((!replicas && !multicast) || (p->bucket_numel && !inplace && !out_slice))
     return fail(COADAPT_E_VALIDATION, "replicas/out_slice is NULL");
   if (!(scale == scale) || std::isinf(scale))
     return fail(COADAPT_E_VALIDATION, "scale must be finite");
   coadapt::dev::RSArgs a;
   std::memset(&a, 0, sizeof(a));
-  for (int q = 0; q < d; ++q) {
-    if (!replicas[q] && p->bucket_numel)
-      return fail(COADAPT_E_VALIDATION, "replica pointer is NULL");
-    if (reinterpret_cast<uintptr_t>(replicas[q]) & 15)
-      return fail(COADAPT_E_VALIDATION, "replica buffers must be 16-byte aligned");
-    a.rep[q] = replicas[q];
+  if (multicast) {
+    if (p->dtype != COADAPT_FP32)
+      return fail(COADAPT_E_VALIDATION,
+                  "NVLS reduction is fp32 only (the switch's bf16/fp16 rounding biases gbar^2)");
+    if (reinterpret_cast<uintptr_t>(multicast) & 15)
+      return fail(COADAPT_E_VALIDATION, "multicast address must be 16-byte aligned");
+    a.mc = multicast;
+    a.nvls = 1;
+  } else {
+    for (int q = 0; q < d; ++q) {
+      if (!replicas[q] && p->bucket_numel)
+        return fail(COADAPT_E_VALIDATION, "replica pointer is NULL");
+      if (reinterpret_cast<uintptr_t>(replicas[q]) & 15)
+        return fail(COADAPT_E_VALIDATION, "replica buffers must be 16-byte aligned");
+      a.rep[q] = replicas[q];
+    }
   }
   if (reinterpret_cast<uintptr_t>(out_slice) & 15)
     return fail(COADAPT_E_VALIDATION, "out_slice must be 16-byte aligned");
@@ -1254,6 +1265,15 @@ int coadapt_gns_allreduce_sqnorm(coadapt_gns* g, const coadapt_plan* p,
   COADAPT_NVTX("coadapt_gns_allreduce_sqnorm");
   return rs_common(g, p, const_cast<const void* const*>(replicas), d, dp_rank,
                    nullptr, true, scale, stream);
+}
+
+int coadapt_gns_nvls_reduce_sqnorm(coadapt_gns* g, const coadapt_plan* p,
+                                   const void* multicast, int d, int dp_rank,
+                                   void* out_slice, double scale, void* stream) {
+  COADAPT_NVTX("coadapt_gns_nvls_reduce_sqnorm");
+  if (!multicast) return fail(COADAPT_E_VALIDATION, "multicast address is NULL");
+  return rs_common(g, p, nullptr, d, dp_rank, out_slice, out_slice == nullptr, scale,
+                   stream, multicast);
 }
 
 int coadapt_nccl_unique_id(void* out, size_t len) {

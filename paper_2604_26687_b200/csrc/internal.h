@@ -105,6 +105,11 @@ struct RSArgs {
   void* out;                      // this rank's slice, element lo at out[0]
   int32_t gslot;
   int32_t inplace;                // 1: write the slice back into every replica
+  // NVLS form (fp32): rep[] unused, the switch reduces every GPU's copy of the
+  // bucket through the multicast address `mc`; inplace stores go back through
+  // `mc` (multimem.st into every GPU's copy)
+  const void* mc;
+  int32_t nvls;
 };
 int occupancy_rs(int dtype);
 cudaError_t launch_rs(int dtype, const Range* full, int nfull, uint64_t lo,

@@ -1133,7 +1133,39 @@ __device__ __forceinline__ void store_dt(char* base, uint64_t i, float x) {
     reinterpret_cast<float*>(base)[i] = x;
 }
 
-template <int DT, int NT, int U>
+// NVLS forms of the loads and stores (fp32 only: the switch adds in fp32)
+__device__ __forceinline__ uint4 mm_ld_reduce_v4(const void* p) {
+  uint4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ float mm_ld_reduce_f32(const void* p) {
+  float r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];"
+               : "=f"(r)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ void mm_st_v4(void* p, const uint4& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st_f32(void* p, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// NVLS = true: the d replicas are one multicast object (the DP group's fp32
+// buckets bound to it, coadapt_nvls_*); every load of the slice is one
+// multimem.ld_reduce (the NVSwitch sums the d copies: each GPU's link carries
+// its slice once instead of (d-1)/d of the bucket), the all-reduce form stores
+// through the multicast address, and gbar^2 is taken from the registers in
+// the same pass.
+template <int DT, int NT, int U, bool NVLS = false>
 __global__ void __launch_bounds__(NT, 2)
     rs_kernel(const Range* __restrict__ R, int nr, uint64_t lo, uint64_t hi,
               const __grid_constant__ RSArgs a, Sink sink) {
@@ -1155,12 +1187,20 @@ __global__ void __launch_bounds__(NT, 2)
       const uint64_t A0 = (pa + PV - 1) / PV * PV, A1 = pb / PV * PV;
       auto scalar = [&](uint64_t i) {
         float s = 0.0f;
-        for (int q = 0; q < a.d; ++q)
-          s = __fadd_rn(s, elem_f32<DT>(reinterpret_cast<uintptr_t>(a.rep[q]) + i * ES));
+        if constexpr (NVLS) {
+          s = mm_ld_reduce_f32(static_cast<const char*>(a.mc) + i * ES);
+        } else {
+          for (int q = 0; q < a.d; ++q)
+            s = __fadd_rn(s, elem_f32<DT>(reinterpret_cast<uintptr_t>(a.rep[q]) + i * ES));
+        }
         const float o = round_dt<DT>(__fmul_rn(s, a.scale));
         if (a.inplace) {
-          for (int q = 0; q < a.d; ++q)
-            store_dt<DT>(static_cast<char*>(const_cast<void*>(a.rep[q])), i, o);
+          if constexpr (NVLS) {
+            mm_st_f32(static_cast<char*>(const_cast<void*>(a.mc)) + i * ES, o);
+          } else {
+            for (int q = 0; q < a.d; ++q)
+              store_dt<DT>(static_cast<char*>(const_cast<void*>(a.rep[q])), i, o);
+          }
         } else {
           store_dt<DT>(out, i - lo, o);
         }
@@ -1180,14 +1220,24 @@ __global__ void __launch_bounds__(NT, 2)
         for (int j = 0; j < U; ++j)
 #pragma unroll
           for (int e = 0; e < PV; ++e) sum[j][e] = 0.0f;
-        for (int q = 0; q < a.d; ++q) {
-          const uint4* src = reinterpret_cast<const uint4*>(
-              static_cast<const char*>(a.rep[q]) + A0 * ES);
+        for (int q = 0; q < (NVLS ? 1 : a.d); ++q) {
           uint4 r[U];
+          if constexpr (NVLS) {
+            const uint4* src = reinterpret_cast<const uint4*>(
+                static_cast<const char*>(a.mc) + A0 * ES);
 #pragma unroll
-          for (int j = 0; j < U; ++j) {
-            const uint64_t v = v0 + (uint64_t)j * NT;
-            r[j] = v < nv ? ld_peer(src + v) : make_uint4(0u, 0u, 0u, 0u);
+            for (int j = 0; j < U; ++j) {
+              const uint64_t v = v0 + (uint64_t)j * NT;
+              r[j] = v < nv ? mm_ld_reduce_v4(src + v) : make_uint4(0u, 0u, 0u, 0u);
+            }
+          } else {
+            const uint4* src = reinterpret_cast<const uint4*>(
+                static_cast<const char*>(a.rep[q]) + A0 * ES);
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+              const uint64_t v = v0 + (uint64_t)j * NT;
+              r[j] = v < nv ? ld_peer(src + v) : make_uint4(0u, 0u, 0u, 0u);
+            }
           }
 #pragma unroll
           for (int j = 0; j < U; ++j) {
@@ -1214,9 +1264,15 @@ __global__ void __launch_bounds__(NT, 2)
           if (a.inplace) {
             // all-reduce form: this rank owns [lo, hi) of every replica, so
             // the position it just read is written back nowhere else
-            for (int q = 0; q < a.d; ++q)
-              st_stream(reinterpret_cast<uint4*>(static_cast<char*>(const_cast<void*>(a.rep[q])) +
-                                                 A0 * ES) + v, ov);
+            if constexpr (NVLS) {
+              mm_st_v4(reinterpret_cast<uint4*>(static_cast<char*>(const_cast<void*>(a.mc)) +
+                                                A0 * ES) + v, ov);
+            } else {
+              for (int q = 0; q < a.d; ++q)
+                st_stream(reinterpret_cast<uint4*>(
+                              static_cast<char*>(const_cast<void*>(a.rep[q])) + A0 * ES) + v,
+                          ov);
+            }
           } else {
             st_stream(reinterpret_cast<uint4*>(out + (A0 - lo) * ES) + v, ov);
           }
@@ -1224,6 +1280,12 @@ __global__ void __launch_bounds__(NT, 2)
         }
       }
     }
+  }
+  if constexpr (NVLS) {
+    // the multicast stores must be visible system-wide before the peers'
+    // stream-ordered barrier lets them read
+    asm volatile("fence.proxy.alias;" ::: "memory");
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
   }
   const double vg = block_sum<NT>(g, red);
   if (threadIdx.x == 0) sink.partials[blockIdx.x] = vg;
@@ -1737,7 +1799,11 @@ int occupancy_accum(int dtype, bool first) {
 
 namespace {
 constexpr int kNTR = 256, kUR = 2;
-void* rs_fn(int dtype) {
+void* rs_fn(int dtype, bool nvls = false) {
+  if (nvls)
+    return dtype == COADAPT_FP32
+               ? reinterpret_cast<void*>(&rs_kernel<COADAPT_FP32, kNTR, kUR, true>)
+               : nullptr;
   switch (dtype) {
     case COADAPT_BF16: return reinterpret_cast<void*>(&rs_kernel<COADAPT_BF16, kNTR, kUR>);
     case COADAPT_FP16: return reinterpret_cast<void*>(&rs_kernel<COADAPT_FP16, kNTR, kUR>);
@@ -1752,7 +1818,7 @@ int occupancy_rs(int dtype) { return occupancy_of(rs_fn(dtype), kNTR); }
 cudaError_t launch_rs(int dtype, const Range* full, int nfull, uint64_t lo,
                       uint64_t hi, const RSArgs& a, Sink sink, int grid,
                       cudaStream_t s) {
-  void* fn = rs_fn(dtype);
+  void* fn = rs_fn(dtype, a.nvls != 0);
   if (!fn) return cudaErrorInvalidValue;
   void* args[] = {(void*)&full, (void*)&nfull, (void*)&lo, (void*)&hi,
                   (void*)&a, (void*)&sink};

@@ -247,6 +247,16 @@ class GnsDevice:
         check(lib().coadapt_gns_allreduce_sqnorm(self.handle, plan.handle, ptrs, k, int(dp_rank),
                                                  float(scale), _stream(stream)))
 
+    def nvls_reduce_sqnorm(self, plan: BucketPlan, bucket: "NvlsBucket", dp_rank: int, scale: float,
+                           out_slice=None, stream=None) -> None:
+        """Switch-reduced DP sync of an fp32 NVLS bucket + gbar^2 of this
+        rank's slice in one pass: reduce-scatter into out_slice, or (out_slice
+        None) all-reduce back into every GPU's copy."""
+        check(lib().coadapt_gns_nvls_reduce_sqnorm(self.handle, plan.handle, C.c_void_p(bucket.multicast),
+                                                   int(bucket.nranks), int(dp_rank),
+                                                   None if out_slice is None else _ptr(out_slice),
+                                                   float(scale), _stream(stream)))
+
     def mean_sqnorm(self, plan: BucketPlan, mean_grad, stream=None) -> None:
         check(lib().coadapt_gns_mean_sqnorm(self.handle, plan.handle, _bucket(plan, mean_grad, "mean_grad"),
                                             _stream(stream)))
