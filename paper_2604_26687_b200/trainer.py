@@ -132,17 +132,17 @@ class GnsManager:
         if self._m != self.M:
             raise L.ValidationError(f"step has {self._m} of {self.M} micro-batches")
         if self.d > 1 and self._nvls is not None:
-            # NVLS: the switch sums the DP group's main_grad (mean), then this
-            # rank's slice of the synchronised main_grad gives its gbar^2 part
-            if self._mean_plan is None:
-                sc = 1.0 / float(self.M) ** 2
-                self._mean_plan = D.BucketPlan([(o, n, w * sc) for o, n, w in self.segments],
-                                               self.numel, L.FP32, self.device,
-                                               slice_index=self.dp_rank, slice_count=self.d)
+            # NVLS: the switch sums the DP group's main_grad (mean) into every
+            # copy, and this rank's slice's gbar^2 part is taken in the same
+            # pass (coadapt_gns_nvls_reduce_sqnorm)
+            if self._ar_plan is None:
+                sc = 1.0 / float(self.M) ** 2  # out = mean over DP; gbar = out / M
+                self._ar_plan = D.BucketPlan([(o, n, w * sc) for o, n, w in self.segments],
+                                             self.numel, L.FP32, self.device)
             self.gns.barrier(stream)
-            self._nvls.allreduce(1.0 / self.d, stream)
+            self.gns.nvls_reduce_sqnorm(self._ar_plan, self._nvls, self.dp_rank, 1.0 / self.d,
+                                        stream=stream)
             self.gns.barrier(stream)
-            self.gns.mean_sqnorm(self._mean_plan, self.main_grad, stream)
         elif self.d > 1 and replicas is not None:
             if len(replicas) != self.d:
                 raise L.ValidationError(f"need {self.d} replicas, got {len(replicas)}")
