@@ -158,3 +158,30 @@ def test_device_face_sequence_vs_oracle(tmp_path):
     res2 = out["d2_result"]
     assert res2["signal"] == pytest.approx(st2.signal, rel=1e-7)
     assert res2["b_simple"] == pytest.approx(st2.noise / st2.signal, rel=1e-7)
+
+
+def _build_step_bench(out):
+    cmd = [CXX, "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "tools", "gns_step_bench.cpp"), "-L", LIBDIR, "-lcoadapt_b200",
+           "-L", "/usr/local/cuda/lib64", "-lcudart",
+           f"-Wl,-rpath,{LIBDIR}", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
+def test_cpp_step_driver_builds(tmp_path):
+    """tools/gns_step_bench.cpp: the whole goodput step from C++ (segments,
+    plans, fused passes with the in-pass finalize, decide) compiles and links"""
+    _build_step_bench(str(tmp_path / "gns_step_bench"))
+
+
+@pytest.mark.gpu
+def test_cpp_step_driver_runs(tmp_path):
+    import json
+    exe = str(tmp_path / "gns_step_bench")
+    _build_step_bench(exe)
+    r = _run(exe, "7b", "1", "2", "1", "4", "3", "2")  # 7B (1,2,1) M=4: small and fast
+    assert r.returncode == 0, r.stdout + r.stderr
+    out = json.loads(r.stdout)
+    assert out["GB_per_s"] > 0 and out["candidates"] > 0
+    assert 100.0 < out["b_simple"] < 1000.0  # phi_true = 256 synthetic gradients
