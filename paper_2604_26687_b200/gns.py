@@ -189,7 +189,25 @@ class Command:
 
 
 def _carr(cands: Sequence[Candidate]):
+    if isinstance(cands, CandidateTable):
+        return cands._arr
     return (L.CandidateC * max(1, len(cands)))(*[c._c() for c in cands])
+
+
+class CandidateTable(Sequence):
+    """A candidate list marshalled for the C-ABI once.  decide() / score /
+    rank accept it in place of a list; the per-step decide then costs one C
+    call (microseconds) instead of rebuilding the ctypes array every step."""
+
+    def __init__(self, cands: Sequence[Candidate]):
+        self._cands = list(cands)
+        self._arr = (L.CandidateC * max(1, len(self._cands)))(*[c._c() for c in self._cands])
+
+    def __len__(self) -> int:
+        return len(self._cands)
+
+    def __getitem__(self, i):
+        return self._cands[i]
 
 
 def synth_candidates(costs: Iterable[tuple], batch_grid: Sequence[int], micro_grid: Sequence[int],

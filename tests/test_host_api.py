@@ -281,3 +281,22 @@ def test_python_wrappers_validate_bucket_tensors():
     host = torch.zeros(64, dtype=torch.bfloat16)
     assert D._bucket(plan, host, host=True) == host.data_ptr()
     assert D._bucket(plan, 1234) == 1234  # raw (e.g. CUDA-IPC) addresses pass through
+
+
+def test_candidate_table_decides_like_the_list():
+    """gns.CandidateTable (marshalled once) gives the same Command, scores
+    and ranking as passing the candidate list."""
+    from paper_2604_26687_b200 import gns as G
+    costs = [(d, t, 8 // (d * t), 1000.0 * d ** 0.5 * (1 + 0.2 * t), 8.0 * d * d + 4.0 * (8 // (d * t)))
+             for d in (1, 2, 4, 8) for t in (1, 2, 4, 8) if 8 % (d * t) == 0]
+    c = G.synth_candidates(costs, [16, 32, 64, 128, 256, 512, 1024, 2048], [1, 2, 4, 8], True)
+    tab = G.CandidateTable(c)
+    assert len(tab) == len(c) and tab[3] == c[3] and list(tab) == c
+    for phi in (None, 3.0, 500.0, 1e5):
+        for cur in (c[0], c[len(c) // 2]):
+            assert G.decide(tab, phi, cur, 1000.0, 900.0, reconfig_cost=40.0) == \
+                G.decide(c, phi, cur, 1000.0, 900.0, reconfig_cost=40.0)
+    assert list(G.score_candidates(tab, 500.0, c[1], 1000.0, 900.0)) == \
+        list(G.score_candidates(c, 500.0, c[1], 1000.0, 900.0))
+    assert G.rank_candidates(tab, 500.0, c[1], 1000.0, 900.0) == \
+        G.rank_candidates(c, 500.0, c[1], 1000.0, 900.0)
