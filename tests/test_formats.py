@@ -1,7 +1,6 @@
 """Wire/disk formats around phi: profile CSV
 (acceptance #10 round trip) and the decision audit
 log."""
-import math
 import os
 
 import pytest

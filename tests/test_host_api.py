@@ -38,7 +38,6 @@ def test_library_exports_every_declared_symbol(L):
 
 def test_reference_headers_declare_the_same_api():
     # our include/coadapt/*.hpp keep every reference declaration (drop-in)
-    import re
     ours = os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "coadapt")
     for h in ("gns.hpp", "goodput.hpp", "strategy.hpp", "io.hpp", "errors.hpp"):
         text = open(os.path.join(ours, h)).read()
