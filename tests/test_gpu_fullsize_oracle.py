@@ -1,4 +1,4 @@
-"""Full-size BASELINE configs C4 and C3 pinned to the CPU oracle.
+"""Full-size BASELINE configs C4, C3 and C2 pinned to the CPU oracle.
 
 Every rank of the job is reduced on the GPU exactly as bench.py does it (C4:
 K1f, one fused pass per rank; C3: K1 per micro-bucket + K2 on the rank's DP
@@ -274,3 +274,70 @@ def test_c3_7b_all_ranks_vs_oracle():
     assert abs(r.b_simple - bs_ref) <= 1e-7 * abs(bs_ref), (r.b_simple, bs_ref)
     # the duplicates were skipped (weight 0 on tp_rank 1 for the norms)
     assert sum(k for l in world for o, k, w in l.segments if w == 0.0) > 0
+
+
+def test_c2_3b_all_ranks_vs_oracle():
+    """C2: Llama-3.2-3B bf16 (8,1,1), M = 8, B_m = 2: every DP rank's 8
+    micro-buckets (3.21 G elements each, 64 in all, 411 GB) through the
+    batched K1 ring and the 8 DP slices of the synchronised mean through K2,
+    against the oracle over the same bytes (round 1 checked this config
+    against a torch fp64 reduction only)."""
+    from paper_2604_26687_b200 import _lib as L
+    from paper_2604_26687_b200 import device as D
+    from paper_2604_26687_b200 import layout as Lay
+    torch.cuda.set_device(0)
+    torch.cuda.empty_cache()
+    spec = Lay.llama32_3b()
+    d, M, Bm, seed = 8, 8, 2, 0xC0905 + 1
+    unit = Lay.noise_unit_for(256.0, Bm)
+    lay = Lay.rank_layout(spec, d, 1, 1, 0)  # t = p = 1: every rank holds the whole model
+    n = lay.numel
+    bufs = [torch.empty(n, dtype=torch.bfloat16, device="cuda") for _ in range(M)]
+    B_g = d * M * Bm
+    g = D.GnsDevice(d, M, B_g, 0)
+    g.begin_step()
+    plan = D.BucketPlan(lay.segments, n, L.BF16, 0)
+    ho = _HostOracle(M)
+    s_ref = np.zeros(d * M)
+
+    def work(arrs, a, b):
+        segs = crop_segments(lay.segments, a, b)
+        return O.fused_sqnorms(arrs, O.BF16, segs, NTH)[0] if segs else np.zeros(M)
+
+    for i_d in range(d):
+        for m in range(M):
+            D.synth_fill(bufs[m], lay.gen, seed, i_d * M + m, Lay.G0, unit)
+        g.micro_sqnorm_batched(plan, bufs, [i_d] * M, list(range(M)))
+        torch.cuda.synchronize()
+        if i_d == 0:
+            _check_generator_window(bufs[:1], lay, [0], seed, unit, (n // 2) & ~7)
+        for s in ho.run(bufs, n, work):
+            s_ref[i_d * M:(i_d + 1) * M] += s
+    mean = bufs[0]
+    D.synth_mean_fill(mean, lay.gen, seed, 0, d * M, Lay.G0, unit)
+    for i_d in range(d):
+        sl = D.BucketPlan(lay.segments, n, L.BF16, 0, slice_index=i_d, slice_count=d)
+        g.mean_sqnorm(sl, mean)
+        torch.cuda.synchronize()
+        sl.close()
+    ho1 = _HostOracle(1)
+
+    def mwork(arrs, a, b):
+        segs = crop_segments(lay.segments, a, b)
+        return O.sqnorm_mt(arrs[0], O.BF16, segs, NTH) if segs else 0.0
+
+    g2_ref = sum(ho1.run([mean], n, mwork))
+    g.finalize(B_g * 2048)
+    r = g.result()
+    parts = g.partials()
+    del bufs, mean
+    torch.cuda.empty_cache()
+    rel_s = np.abs(parts[:-1] - s_ref) / s_ref
+    st = O.finalize_step(s_ref, g2_ref, B_g)
+    print(f"C2: max rel s {rel_s.max():.3e}, rel gbar2 {abs(parts[-1] - g2_ref) / g2_ref:.3e}, "
+          f"B_simple gpu {r.b_simple!r} oracle {st.noise / st.signal!r}")
+    assert rel_s.max() <= 1e-9, (rel_s.max(), parts[:-1], s_ref)
+    assert abs(parts[-1] - g2_ref) <= 1e-9 * g2_ref, (parts[-1], g2_ref)
+    assert abs(r.stats.signal - st.signal) <= 1e-7 * abs(st.signal)
+    bs_ref = st.noise / st.signal
+    assert abs(r.b_simple - bs_ref) <= 1e-7 * abs(bs_ref), (r.b_simple, bs_ref)
