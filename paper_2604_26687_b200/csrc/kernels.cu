@@ -1686,10 +1686,19 @@ TmaFn tma_fn_v() {
 // whose 8-warp groups leave 32 threads idle).
 constexpr int kBestShape[17] = {4, 4, 4, 0, 4, 4, 0, 4, 0, 4, 5, 5, 0, 0, 4, 5, 5};
 
+#ifndef COADAPT_SHAPE_SWEEP
+#define COADAPT_SHAPE_SWEEP 0  // 1: every shape selectable by COADAPT_TMA_SHAPE
+#endif
+
 template <int DT, int M>
 TmaFn tma_fn(bool mean) {
   // batched K1 (no mean term): the best shape only
   if (!mean) return tma_fn_v<DT, M, kBestShape[M], false>();
+#if !COADAPT_SHAPE_SWEEP
+  // shipped build: the measured best shape per M only (the sweep build,
+  // -DCOADAPT_SHAPE_SWEEP=1, instantiates all of them: 5x the compile time)
+  return tma_fn_v<DT, M, kBestShape[M], true>();
+#else
   static const char* e = getenv("COADAPT_TMA_SHAPE");  // development sweep
   switch (e ? atoi(e) : kBestShape[M]) {
     case 1: return tma_fn_v<DT, M, 1, true>();
@@ -1699,6 +1708,7 @@ TmaFn tma_fn(bool mean) {
     case 5: return tma_fn_v<DT, M, 5, true>();
     default: return tma_fn_v<DT, M, 0, true>();
   }
+#endif
 }
 
 template <int DT>

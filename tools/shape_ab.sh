@@ -1,5 +1,6 @@
 #!/bin/bash
-# A/B/A/B of K1f launch shapes (COADAPT_TMA_SHAPE) on one box under sustained
+# A/B/A/B of K1f launch shapes (COADAPT_TMA_SHAPE; needs a library built with
+# make EXTRA_NVFLAGS=-DCOADAPT_SHAPE_SWEEP=1) on one box under sustained
 # load, with power / SM clock sampling: gpurun_out/<TAG>_s<shape>_r<round>.*
 S=${S:-6}; ROUNDS=${ROUNDS:-2}; TAG=${TAG:-shape}; M=${M:-16}
 mkdir -p gpurun_out
