@@ -299,3 +299,16 @@ def test_candidate_table_decides_like_the_list():
         list(G.score_candidates(c, 500.0, c[1], 1000.0, 900.0))
     assert G.rank_candidates(tab, 500.0, c[1], 1000.0, 900.0) == \
         G.rank_candidates(c, 500.0, c[1], 1000.0, 900.0)
+
+
+def test_round2_entry_points_validate_without_a_device():
+    """The round-2 C-ABI entry points reject bad arguments with status 1
+    before touching a device (usable as a CPU-side contract check)."""
+    import ctypes as C
+    from paper_2604_26687_b200 import _lib as LL
+    lib = LL.lib()
+    ptrs = (C.c_void_p * 1)()
+    assert lib.coadapt_gns_fused_sqnorm_finalize(None, None, ptrs, 1, 2048, None) == LL.E_VALIDATION
+    assert lib.coadapt_gns_mean_sqnorm_finalize(None, None, None, 2048, None) == LL.E_VALIDATION
+    assert lib.coadapt_gns_nvls_reduce_sqnorm(None, None, None, 2, 0, None, 0.5, None) == LL.E_VALIDATION
+    assert b"NULL" in lib.coadapt_last_error()
