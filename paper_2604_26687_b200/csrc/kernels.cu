@@ -918,6 +918,9 @@ __device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
                : "memory");
 }
 
+#ifndef COADAPT_KA_NO_NORM
+#define COADAPT_KA_NO_NORM 0
+#endif
 template <int DT>
 __device__ __forceinline__ void accum_elem(float* mg, float g, double w,
                                            bool first, bool mean, double& s,
@@ -1020,11 +1023,15 @@ __global__ void __launch_bounds__(NT, 3)
               gd = f[e];
             }
             mf[e] = nvf;
+#if !COADAPT_KA_NO_NORM  // (1: the plain accumulation, for the overhead A/B)
             if (e & 1) a1 = fma(gd, gd, a1); else a0 = fma(gd, gd, a0);
             if (mean) {
               const double nd = nvf;
               if (e & 1) m1 = fma(nd, nd, m1); else m0 = fma(nd, nd, m0);
             }
+#else
+            (void)gd;
+#endif
           }
 #pragma unroll
           for (int h = 0; h < PV / 4; ++h) st_stream(mv + v * (PV / 4) + h, mr[j][h]);
