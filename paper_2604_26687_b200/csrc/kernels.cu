@@ -116,14 +116,16 @@ __device__ __forceinline__ double f16_f64(uint16_t h) {
   return d;
 }
 // s + x in one fp32 rounding, x a bf16 half-word read in place (SASS
-// FHFMA.BF16, x * 1.0 + s): identical to __fadd_rn(s, (float)x).
+// FHADD.BF16, the mixed-precision add): identical to __fadd_rn(s, (float)x).
+// (Round 1 used FHFMA.BF16, x * 1.0 + s — same result; FHADD measured
+// +0.4 % on the fused pass, profiles/r02_vacc_variants.txt call 13.)
 __device__ __forceinline__ float bf16_addf(float s, uint16_t h) {
-  asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(s) : "h"(h), "h"((uint16_t)0x3F80));
+  asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(s) : "h"(h));
   return s;
 }
 
 // sum[e] += x_e (fp32, one rounding each) for the values of one vector: the
-// micro-batch sum of the fused pass.  bf16 via FHFMA on the packed halves,
+// micro-batch sum of the fused pass.  bf16 via FHADD on the packed halves,
 // the others unpacked and added pairwise with FADD2 (same rounding per lane).
 template <int DT>
 __device__ __forceinline__ void micro_add(const uint4& v, float* sum) {
@@ -1012,7 +1014,7 @@ __global__ void __launch_bounds__(NT, 3)
             float nvf;
             double gd;
             if constexpr (DT == COADAPT_BF16) {
-              // bf16 halves read in place: FHFMA.BF16 for the fp32 add (one
+              // bf16 halves read in place: FHADD.BF16 for the fp32 add (one
               // rounding, == __fadd_rn), F2F.F64.BF16 for the square
               const uint16_t h = (e & 1) ? (uint16_t)(gw[e >> 1] >> 16)
                                          : (uint16_t)(gw[e >> 1] & 0xffffu);
