@@ -150,115 +150,19 @@ __device__ __forceinline__ void micro_add(const uint4& v, float* sum) {
   }
 }
 
-// bf16 -> fp64 without the XU: the bits of a bf16 x placed in an fp64's high
-// word (sign dropped, it is squared) read as x * 2^-896 exactly — zero and
-// subnormals included — and with 1792 added to the exponent field as
-// x * 2^896 (exact for every normal x), so x^2 = a * c exactly and
-// DFMA(a, c, acc) == DFMA(x, x, acc) bit for bit.  For a bf16 subnormal
-// (|x| < 2^-126) c lacks the implicit-bit correction and a * c is off by
-// less than 2^-251 (absolute): below half an ulp of any accumulator above
-// 2^-190, i.e. invisible unless the whole sum is that small.  One shift and
-// two LOP3 per element on the ALU pipe instead of one F2F on the quarter-
-// rate XU pipe.
-#ifndef COADAPT_VACC
-#define COADAPT_VACC 0  // 0: F2F (XU) for every element, 1: ALU-built, 2: half/half
-#endif
-__device__ __forceinline__ void bf16_lo_ac(uint32_t w, double& a, double& c) {
-  const uint32_t t = w << 13;  // low half's exponent+mantissa -> bits 20..27 / 13..19
-  a = __hiloint2double(t & 0x0FFFE000u, 0);
-  c = __hiloint2double((t & 0x0FFFE000u) | 0x70000000u, 0);
-}
-__device__ __forceinline__ void bf16_hi_ac(uint32_t w, double& a, double& c) {
-  const uint32_t t = w >> 3;   // high half's exponent+mantissa -> same positions
-  a = __hiloint2double(t & 0x0FFFE000u, 0);
-  c = __hiloint2double((t & 0x0FFFE000u) | 0x70000000u, 0);
-}
-
-// One operand instead of two: the exponent field offset by 485 (an integer
-// add) makes the fp64 x * 2^-411 for every normal x, and maps x = 0 to
-// 2^-538, whose square (2^-1076) rounds away in any fp64 sum — so DFMA(a, a,
-// acc_s) accumulates sum x^2 * 2^-822, exactly the unscaled RN(acc + x^2)
-// scaled by a power of two while the partial sum stays a normal fp64 (true
-// sum >= 2^-200); the caller rescales the total by 2^822 (exact).  bf16
-// subnormals contribute < 2^-252 (absolute) each.
-constexpr uint32_t kExp485 = 485u << 20;
-__device__ __forceinline__ double bf16_lo_s(uint32_t w) {
-  return __hiloint2double(((w << 13) & 0x0FFFE000u) + kExp485, 0);
-}
-__device__ __forceinline__ double bf16_hi_s(uint32_t w) {
-  return __hiloint2double(((w >> 3) & 0x0FFFE000u) + kExp485, 0);
-}
-
-// fp32 -> fp64 pair for an exact square without the XU: the fp32 bits moved
-// into fp64 position read as s * 2^-896 (zero and subnormals included), and
-// with 1792 added to the exponent field as s * 2^896 (every normal s); the
-// low 3 mantissa bits land in the low word, shared by both.  a * c == s * s
-// exactly (24 x 24 bits), so DFMA(a, c, g) == DFMA(s, s, g) bit for bit;
-// only an fp32-subnormal s (|s| < 2^-126) is off, by < 2^-251 absolute.
-#ifndef COADAPT_GSQ
-#define COADAPT_GSQ 0  // 1: measured 1.3 % slower sustained (profiles/r02_vacc_variants.txt)
-#endif
-__device__ __forceinline__ void f32_ac(float s, double& a, double& c) {
-  const uint32_t b = __float_as_uint(s);
-  const uint32_t hi = (b >> 3) & 0x0FFFFFFFu, lo = b << 29;
-  a = __hiloint2double(hi, lo);
-  c = __hiloint2double(hi | 0x70000000u, lo);
-}
-
 // acc += sum of squares of one vector, every square exact in fp64.
 // Each value goes to fp64 with one F2F on the XU pipe (bf16 straight from
-// the half-word), which with the 1 kW power cap is what bounds these
-// kernels.  Measured alternatives (profiles/r01c_vacc_variants.txt): fp32
-// squares summed in runs of 8 (+7 % K1f, +22 % K1 sustained) is not exact;
-// building the fp64 from integer ops (half or all of the elements) moves no
-// sustained number.  Exactness was kept.
+// the half-word) and is squared into one of two DFMA chains.  Measured
+// alternatives (profiles/r01c_vacc_variants.txt, r02_vacc_variants.txt):
+// fp32 squares summed in runs of 8 (+7 % K1f, +22 % K1 sustained) are not
+// exact; every exact XU-free form (fp64 built from the bits on the ALU, as
+// two scaled operands or one into a 2^-822-scaled accumulator, for half or
+// all of the elements) moves K1 by at most +1.5 % and costs the fused pass
+// 12-16 %; a chain continuing the accumulator costs 1.2 %.  This form stays.
 template <int DT>
 __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
   if constexpr (DT == COADAPT_BF16) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#if COADAPT_VACC == 1
-    double a0, c0, a1, c1;
-    bf16_lo_ac(w[0], a0, c0);
-    bf16_hi_ac(w[0], a1, c1);
-    a0 *= c0;
-    a1 *= c1;
-#pragma unroll
-    for (int i = 1; i < 4; ++i) {
-      double x0, y0, x1, y1;
-      bf16_lo_ac(w[i], x0, y0);
-      bf16_hi_ac(w[i], x1, y1);
-      a0 = fma(x0, y0, a0);
-      a1 = fma(x1, y1, a1);
-    }
-#elif COADAPT_VACC == 3
-    // scaled by 2^-822 (see bf16_lo_s); one register per element
-    double a0 = bf16_lo_s(w[0]);
-    double a1 = bf16_hi_s(w[0]);
-    a0 *= a0;
-    a1 *= a1;
-#pragma unroll
-    for (int i = 1; i < 4; ++i) {
-      const double d0 = bf16_lo_s(w[i]);
-      const double d1 = bf16_hi_s(w[i]);
-      a0 = fma(d0, d0, a0);
-      a1 = fma(d1, d1, a1);
-    }
-#elif COADAPT_VACC == 2
-    // low halves on the ALU, high halves through F2F (both pipes in use)
-    double a0, c0;
-    bf16_lo_ac(w[0], a0, c0);
-    double a1 = bf16_f64((uint16_t)(w[0] >> 16));
-    a0 *= c0;
-    a1 *= a1;
-#pragma unroll
-    for (int i = 1; i < 4; ++i) {
-      double x0, y0;
-      bf16_lo_ac(w[i], x0, y0);
-      const double d1 = bf16_f64((uint16_t)(w[i] >> 16));
-      a0 = fma(x0, y0, a0);
-      a1 = fma(d1, d1, a1);
-    }
-#else
     // two fp64 chains per vector halve the dependent DFMA latency
     double a0 = bf16_f64((uint16_t)(w[0] & 0xffffu));
     double a1 = bf16_f64((uint16_t)(w[0] >> 16));
@@ -271,7 +175,6 @@ __device__ __forceinline__ void vacc(const uint4& v, double& acc) {
       a0 = fma(d0, d0, a0);
       a1 = fma(d1, d1, a1);
     }
-#endif
     acc += a0 + a1;
     return;
   }
@@ -763,14 +666,8 @@ __device__ __forceinline__ void tma_consume_cols(const char* stage,
       double g = 0.0;
 #pragma unroll
       for (int e = 0; e < C::PV; ++e) {
-#if COADAPT_GSQ
-        double a, c;
-        f32_ac(sum[e], a, c);
-        g = fma(a, c, g);
-#else
         const double sd = sum[e];
         g = fma(sd, sd, g);
-#endif
       }
       gacc = WEIGHTED ? fma(w, g, gacc) : gacc + g;
     }
