@@ -360,6 +360,7 @@ def run_ours(args):
     launch_bytes = [pl.active_elements * es * M for pl in plans]
 
     ev_pairs, tail_pairs, decide_s = [], [], []
+    mean_pairs, step_marks = [], []  # K2 launches; (step start, last launch end) per step
 
     # in-pass: the step's last reduction launch finalizes in its last CTA
     # (after the NVLink slot exchange when N > 1) — north_star item 2
@@ -367,6 +368,9 @@ def run_ours(args):
     tokens = B_g * SEQ_LEN
 
     def step(timed):
+        if timed:
+            s0 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
         g.begin_step(stream)
         for i, pl in enumerate(plans):
             last = inpass and i + 1 == len(plans)
@@ -387,10 +391,17 @@ def run_ours(args):
                 # kept out of the kernel roofline
                 ev_pairs.append((e0, e1, launch_bytes[i], not (last and fused and ws > 1)))
             if not fused:
+                if timed:
+                    m0 = torch.cuda.Event(enable_timing=True)
+                    m1 = torch.cuda.Event(enable_timing=True)
+                    m0.record(stream)
                 if last:
                     g.mean_sqnorm_finalize(slices[i], mean, tokens, stream)
                 else:
                     g.mean_sqnorm(slices[i], mean, stream)
+                if timed:
+                    m1.record(stream)
+                    mean_pairs.append((m0, m1))
         if timed:
             f0 = torch.cuda.Event(enable_timing=True)
             f1 = torch.cuda.Event(enable_timing=True)
@@ -404,6 +415,7 @@ def run_ours(args):
         if timed:
             f1.record(stream)
             tail_pairs.append((f0, f1))
+            step_marks.append((s0, f1))
         r = g.result()  # phi -> host (waits for this step)
         h0 = time.perf_counter()
         G.decide(cands, r.phi if r.phi_available else None, current, 1000.0, 900.0, reconfig_cost=40.0)
@@ -427,6 +439,8 @@ def run_ours(args):
     ro_peak = 3 * probe_bytes / (pe0.elapsed_time(pe1) / 1e3) / 1e9
 
     clocks = ClockSampler(dev)
+    if os.environ.get("COADAPT_BENCH_NO_CLOCKS") == "1":  # diagnosis only: no sampler
+        clocks.start = lambda: None
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -453,6 +467,11 @@ def run_ours(args):
     # the all-reduce + finalize tail on the device, the host decide()
     red_ms = sum(a.elapsed_time(b) for a, b, _, _ in ev_pairs) / args.steps
     tail_ms = sum(a.elapsed_time(b) for a, b in tail_pairs) / max(1, len(tail_pairs))
+    mean_ms = sum(a.elapsed_time(b) for a, b in mean_pairs) / args.steps
+    # the stream's idle time between steps (phi D2H, host wake-up, decide,
+    # the next step's first launch): last launch end -> next step start
+    idle = [step_marks[k][1].elapsed_time(step_marks[k + 1][0]) for k in range(len(step_marks) - 1)]
+    idle_ms = sum(idle) / len(idle) if idle else 0.0
     red_all = [red_ms]
     if ws > 1:  # per-GPU reduction time: the max-over-ranks step waits for the slowest
         rt = torch.tensor([red_ms], dtype=torch.float64, device="cuda")
@@ -489,6 +508,9 @@ def run_ours(args):
         synced_ms = float(tt.item())
     goodput_step = {"step_ms": round(ms, 4), "reductions_ms": round(red_ms, 4),
                     "reductions_ms_per_gpu": [round(x, 4) for x in red_all],
+                    "mean_slices_ms": round(mean_ms, 4) if not fused else None,
+                    "between_steps_idle_ms": round(idle_ms, 4),
+                    "between_steps_idle_ms_each": [round(x, 3) for x in idle],
                     "rank_skew_ms": round(max(red_all) - min(red_all), 4),
                     "allreduce_finalize_ms": round(tail_ms, 4),
                     "allreduce_finalize_ms_synced": round(synced_ms, 4),
