@@ -640,3 +640,38 @@ def test_batched_k1_tma_ring_matches_single_passes(D, L, dtype, M):
         for m in (0, M - 1):
             ref = O.sqnorm(_host_u(bufs[m]), dtype, segs)
             assert _rel(pb[M + m], ref) <= RTOL_NORM
+
+
+@pytest.mark.parametrize("dtype", [0, 1, 2])
+def test_every_m_instantiation_matches_oracle(D, L, dtype):
+    """Each micro-batch count M = 2..16 is its own fused_tma_kernel
+    instantiation (shape chosen per M, kBestShape), for the fused pass and
+    for the batched K1 ring: every one against the oracle, on a bucket long
+    enough for several chunks per CTA and with a weight-0 hole that cuts a
+    tile."""
+    numel = 148 * 3584 * 3 + 1234
+    segs = [(0, 500_000, 1.0), (500_000, 7777, 0.0), (507_777, numel - 507_777, 1.0)]
+    gen = [(0, numel, 0, numel, numel)]
+    unit = O.noise_unit_for(2 ** -10, 256.0, 1)
+    bufs = [_dev_buf(D, numel, dtype, gen, 404, m, unit)[1] for m in range(16)]
+    host = [_host_u(b) for b in bufs]
+    plan = D.BucketPlan(segs, numel, dtype, 0)
+    for M in range(2, 17):
+        g = D.GnsDevice(1, M, M, 0)
+        g.begin_step()
+        g.fused_sqnorm(plan, bufs[:M])
+        parts = g.partials()
+        s, ss = O.fused_sqnorms(host[:M], dtype, segs, 4)
+        for m in range(M):
+            assert _rel(parts[m], s[m]) <= RTOL_NORM, (M, m)
+        assert _rel(parts[M], ss / (M * M)) <= RTOL_NORM, M
+        g.close()
+        gb = D.GnsDevice(2, M, 2 * M, 0)
+        gb.begin_step()
+        gb.micro_sqnorm_batched(plan, bufs[:M], [0] * M, list(range(M)))
+        pb = gb.partials()
+        for m in range(M):
+            assert _rel(pb[m], s[m]) <= RTOL_NORM, ("batched", M, m)
+        assert np.all(pb[M:] == 0.0)
+        gb.close()
+    plan.close()
