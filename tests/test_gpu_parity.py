@@ -675,3 +675,57 @@ def test_every_m_instantiation_matches_oracle(D, L, dtype):
         assert np.all(pb[M:] == 0.0)
         gb.close()
     plan.close()
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), -float("inf")])
+@pytest.mark.parametrize("form", ["fused", "inpass", "batched", "accumulate"])
+def test_nonfinite_in_every_reduction_form(D, L, bad, form):
+    """A non-finite element in a counted range makes the step a validation
+    error (finalize leaves the state untouched) whatever reduction carried it
+    — the fused TMA pass, its in-pass finalize, the batched K1 ring, the
+    trainer form — while the same value inside a weight-0 range (a TP
+    duplicate, never loaded) changes nothing."""
+    n = 148 * 3584 + 4096
+    M = 4
+    hole = (200_000, 4096)
+    segs = [(0, hole[0], 1.0), (hole[0], hole[1], 0.0), (hole[0] + hole[1], n - hole[0] - hole[1], 1.0)]
+    plan = D.BucketPlan(segs, n, L.BF16, 0)
+    for where, expect_error in ((123_457, True), (hole[0] + 100, False)):
+        bufs = [torch.full((n,), 0.5, dtype=torch.bfloat16, device="cuda") for _ in range(M)]
+        bufs[2][where] = bad
+        d = 2 if form == "batched" else 1
+        g = D.GnsDevice(d, M, d * M, 0)
+        st0 = g.get_state().as_tuple()
+        g.begin_step()
+        if form == "fused":
+            g.fused_sqnorm(plan, bufs)
+            g.finalize(M * 2048)
+        elif form == "inpass":
+            g.fused_sqnorm_finalize(plan, bufs, M * 2048)
+        elif form == "batched":
+            g.micro_sqnorm_batched(plan, bufs, [0] * M, list(range(M)))
+            g.micro_sqnorm_batched(plan, [torch.full_like(bufs[0], 0.5)] * M, [1] * M, list(range(M)))
+            sl0 = D.BucketPlan(segs, n, L.BF16, 0, slice_index=0, slice_count=2)
+            sl1 = D.BucketPlan(segs, n, L.BF16, 0, slice_index=1, slice_count=2)
+            mean = torch.full((n,), 0.5, dtype=torch.bfloat16, device="cuda")
+            g.mean_sqnorm(sl0, mean)
+            g.mean_sqnorm(sl1, mean)
+            g.finalize(d * M * 2048)
+        else:
+            main = torch.zeros(n, dtype=torch.float32, device="cuda")
+            for m in range(M):
+                g.accumulate(plan, main, bufs[m], 0, m, first=m == 0, last_mean=m == M - 1)
+            g.finalize(M * 2048)
+        if expect_error:
+            with pytest.raises(L.ValidationError):
+                g.result()
+            assert g.get_state().as_tuple() == st0
+        else:
+            r = g.result()
+            assert r.status == 0
+            parts = g.partials()
+            assert np.all(np.isfinite(parts))
+            counted = n - hole[1]
+            assert parts[0] == 0.25 * counted  # 0.5^2 per counted element, exact
+        g.close()
+    plan.close()
