@@ -109,6 +109,8 @@ class GnsDevicePlan {
   void allreduce(void* stream);
   void finalize(std::int64_t tokens_this_step, void* stream);
   DeviceStepResult result();
+  // non-blocking: true once result() would return without waiting
+  bool result_ready();
   // the N recorded values as the reference's StepAccumulator
   StepAccumulator accumulator();
   GnsState state();

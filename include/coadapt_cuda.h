@@ -22,7 +22,8 @@
  *    thread-local message of the last failure on the calling thread.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *    stream).  All device work is asynchronous on that stream; only
- *    coadapt_gns_read_result / coadapt_gns_read_partials block.
+ *    coadapt_gns_read_result / coadapt_gns_read_partials block
+ *    (coadapt_gns_result_ready polls without blocking).
  *  - device gradient buffers are borrowed (like std::span): the library never
  *    frees or retains them past the call's stream work.  Host buffers given
  *    to coadapt_gns_fused_sqnorm_host must stay valid until that stream work
@@ -374,6 +375,14 @@ int coadapt_gns_mean_sqnorm_finalize(coadapt_gns* g, const coadapt_plan* p,
                                      int64_t tokens_this_step, void* stream);
 /* waits for the last finalize and returns its result */
 int coadapt_gns_read_result(coadapt_gns* g, coadapt_gns_result* out);
+/* non-blocking: *ready = 1 once the last finalize's result has reached the
+ * host (coadapt_gns_read_result then returns without waiting), 0 while the
+ * step is still running.  Lets a trainer enqueue its optimizer step and the
+ * next forward before it reads phi (the GNS never stalls the stream); the
+ * result must be read before the next finalize is enqueued, which reuses
+ * the host buffer.  Replaces nothing in the reference (its finalize_step is
+ * synchronous, gns.hpp:42-49). */
+int coadapt_gns_result_ready(coadapt_gns* g, int* ready);
 /* synchronous read of the N+1 slots (s values, then gbar^2) */
 int coadapt_gns_read_partials(coadapt_gns* g, double* out, size_t n);
 /* checkpoint / restore of the device GnsState (synchronous) */

@@ -212,6 +212,7 @@ SIGNATURES = {
     "coadapt_gns_fused_sqnorm_finalize": (I, [P, P, P, I, I64, P]),
     "coadapt_gns_mean_sqnorm_finalize": (I, [P, P, P, I64, P]),
     "coadapt_gns_read_result": (I, [P, P]),
+    "coadapt_gns_result_ready": (I, [P, P]),
     "coadapt_gns_read_partials": (I, [P, P, SZ]),
     "coadapt_gns_get_state": (I, [P, P]),
     "coadapt_gns_set_state": (I, [P, P]),

@@ -1462,6 +1462,21 @@ int coadapt_gns_read_result(coadapt_gns* g, coadapt_gns_result* out) {
   return COADAPT_OK;
 }
 
+int coadapt_gns_result_ready(coadapt_gns* g, int* ready) {
+  if (!g || !ready) return fail(COADAPT_E_VALIDATION, "gns/ready is NULL");
+  if (!g->finalized)
+    return fail(COADAPT_E_VALIDATION, "no finalized step to query");
+  GUARD(g->device);
+  const cudaError_t e = cudaEventQuery(g->result_ready);
+  if (e == cudaErrorNotReady) {
+    *ready = 0;
+    return COADAPT_OK;
+  }
+  CU(e);
+  *ready = 1;
+  return COADAPT_OK;
+}
+
 int coadapt_gns_read_partials(coadapt_gns* g, double* out, size_t n) {
   if (!g || !out) return fail(COADAPT_E_VALIDATION, "gns/out is NULL");
   if (n < (size_t)g->N + 1)

@@ -217,6 +217,12 @@ DeviceStepResult GnsDevicePlan::result() {
   return o;
 }
 
+bool GnsDevicePlan::result_ready() {
+  int ready = 0;
+  check(coadapt_gns_result_ready(g_, &ready));
+  return ready != 0;
+}
+
 StepAccumulator GnsDevicePlan::accumulator() {
   std::vector<double> v((std::size_t)dp_ * micro_ + 1);
   check(coadapt_gns_read_partials(g_, v.data(), v.size()));

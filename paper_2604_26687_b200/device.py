@@ -291,6 +291,12 @@ class GnsDevice:
         check(lib().coadapt_gns_read_result(self.handle, C.byref(r)))
         return r
 
+    def result_ready(self) -> bool:
+        """Non-blocking: has the last finalize's result reached the host?"""
+        ready = C.c_int(0)
+        check(lib().coadapt_gns_result_ready(self.handle, C.byref(ready)))
+        return bool(ready.value)
+
     def partials(self) -> np.ndarray:
         out = np.zeros(self.n + 1, np.float64)
         check(lib().coadapt_gns_read_partials(self.handle, out.ctypes.data, out.size))

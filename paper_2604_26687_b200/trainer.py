@@ -29,6 +29,10 @@ Usage::
         r = mgr.finish_step(tokens=B_g * seq_len)  # r.phi, r.stats, r.state
         optimizer_step_on(mgr.main_grad)
 
+    or, without a host sync per step: ``mgr.finish_step(tokens, wait=False)``,
+    the optimizer step, then ``mgr.poll()`` / ``mgr.result()`` before the
+    next ``finish_step``.
+
 Do not call ``zero_grad(set_to_none=True)`` on the model: the manager owns
 the grad views and clears the bucket after each micro-batch.
 """
@@ -122,13 +126,18 @@ class GnsManager:
         self._m = m + 1
 
     def finish_step(self, tokens: int, synced_main_grad: Optional[torch.Tensor] = None,
-                    replicas=None, stream=None) -> L.GnsResult:
+                    replicas=None, stream=None, wait: bool = True) -> Optional[L.GnsResult]:
         """All-reduce the slots (if attached), finalize, read φ.  For d > 1
         either pass the DP-summed main_grad (this rank reads its slice of
         it) or ``replicas`` — the d ranks' main_grad buckets in DP order
         (peer pointers; this rank's own tensor or pointer at dp_rank): the
         DP all-reduce (mean) of main_grad and ḡ² then run as one NVLink pass,
-        bracketed by stream-ordered barriers."""
+        bracketed by stream-ordered barriers.
+
+        ``wait=False`` enqueues everything and returns None without
+        blocking: the host goes on to enqueue the optimizer step and the
+        next forward while the GPU finishes, and reads φ with ``poll()`` or
+        ``result()`` any time before the next ``finish_step``."""
         if self._m != self.M:
             raise L.ValidationError(f"step has {self._m} of {self.M} micro-batches")
         if self.d > 1 and self._nvls is not None:
@@ -164,4 +173,13 @@ class GnsManager:
             self.gns.mean_sqnorm(self._mean_plan, synced_main_grad, stream)
         self.gns.allreduce(stream)
         self.gns.finalize(int(tokens), stream)
+        return self.gns.result() if wait else None
+
+    def poll(self) -> Optional[L.GnsResult]:
+        """The last finished step's result if it has reached the host, else
+        None (never blocks)."""
+        return self.gns.result() if self.gns.result_ready() else None
+
+    def result(self) -> L.GnsResult:
+        """The last finished step's result (waits for it)."""
         return self.gns.result()

@@ -146,6 +146,8 @@ int main(int argc, char** argv) {
         gns.record_fused(layout, ptrs, stream);
         gns.allreduce(stream);  // world 1: the local sum
         gns.finalize((std::int64_t)M * Bm * 2048, stream);
+        while (!gns.result_ready()) {
+        }  // non-blocking poll until the step's result is on the host
         const DeviceStepResult r = gns.result();
         bad |= check_against_host(gns, r, host_state, (std::int64_t)M * Bm * 2048, "d=1");
         if (step == 1) {

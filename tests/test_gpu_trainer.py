@@ -134,3 +134,48 @@ def test_manager_d2_nvlink_allreduce_form():
     assert np.allclose(tot[:-1], s_ref, rtol=1e-12, atol=0)
     g2_ref = float((mean_ref.double() ** 2).sum()) / M ** 2
     assert abs(tot[-1] - g2_ref) <= 1e-12 * g2_ref
+
+
+def test_finish_step_without_host_sync():
+    """finish_step(wait=False) enqueues the step and returns at once; the
+    result is not ready while the stream is still busy (a sleep kernel queued
+    ahead of it), poll() never blocks, and once the stream drains the result
+    equals the blocking form's, bit for bit, over several steps."""
+    from paper_2604_26687_b200.trainer import GnsManager
+    M = 4
+    xs, ys = _data(M, 5)
+    mods = [_model(3), _model(3)]
+    mgrs = [GnsManager(m.parameters(), micro_count=M, global_batch=M * 8) for m in mods]
+    for step in range(3):
+        for k, (model, mgr) in enumerate(zip(mods, mgrs)):
+            mgr.begin_step()
+            for x, y in zip(xs, ys):
+                torch.nn.functional.mse_loss(model(x).float(), y.float()).backward()
+                mgr.after_backward()
+            if k == 0:
+                blocking = mgr.finish_step(tokens=M * 8 * 2048)
+            else:
+                torch.cuda._sleep(200_000_000)  # ~0.1 s of GPU time queued ahead
+                assert mgr.finish_step(tokens=M * 8 * 2048, wait=False) is None
+                assert not mgr.gns.result_ready() and mgr.poll() is None
+                torch.cuda.synchronize()
+                assert mgr.gns.result_ready()
+                polled = mgr.poll()
+                assert polled is not None
+                r = mgr.result()
+                for a in (polled, r):
+                    assert a.state.as_tuple() == blocking.state.as_tuple()
+                    assert (a.stats.signal, a.stats.noise, a.b_simple) == \
+                        (blocking.stats.signal, blocking.stats.noise, blocking.b_simple)
+            # the optimizer step would go here; keep both models identical
+    for mgr in mgrs:
+        mgr.gns.close()
+
+
+def test_result_ready_before_any_finalize_is_an_error():
+    from paper_2604_26687_b200 import _lib as L
+    from paper_2604_26687_b200 import device as D
+    g = D.GnsDevice(1, 2, 2, 0)
+    with pytest.raises(L.ValidationError):
+        g.result_ready()
+    g.close()
