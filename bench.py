@@ -546,6 +546,17 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         E = min(args.e2e_elems, numel)
+        # pinned host sample of every rank on this box: at most a quarter of
+        # the host RAM and 16 GiB in total (8 ranks x 16 buckets x 268 MB
+        # would pin 34 GB); the metric is a rate, so a smaller sample per
+        # rank changes nothing but the step length
+        try:
+            import psutil
+            cap = min(16 << 30, psutil.virtual_memory().total // 4)
+            per_elem = (M + (0 if fused else 1)) * es * ws
+            E = min(E, max(1 << 22, cap // per_elem // 64 * 64))
+        except ImportError:
+            pass
         segs_e = [(o, min(n, E - o), w) for o, n, w in mine[0].segments if o < E]
         plan_e = D.BucketPlan(segs_e, E, dt, dev)
         host = [pool[m][:E].cpu().pin_memory() for m in range(M)]
