@@ -155,6 +155,19 @@ int main(int argc, char** argv) {
   }
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   std::vector<std::vector<void*>> scratch(n);
+  std::vector<std::vector<cudaStream_t>> pst(n);  // one stream per peer (mode 4)
+  std::vector<std::vector<cudaEvent_t>> pev(n);
+  for (int d = 0; d < n; ++d) {
+    CK(cudaSetDevice(d));
+    for (int k = 0; k < n - 1; ++k) {
+      cudaStream_t s;
+      cudaEvent_t e;
+      CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      pst[d].push_back(s);
+      pev[d].push_back(e);
+    }
+  }
   auto run = [&](int mode, int peers_per_gpu, int reps) -> double {
     // each GPU reads from `peers_per_gpu` peers (d+1, d+2, ...); returns
     // the slowest GPU's peer GB/s received
@@ -176,13 +189,28 @@ int main(int argc, char** argv) {
         else if (mode == 2)
           tma_read<<<sms, 256, kTile * kStages, st[d]>>>(P, B, sink[d]);
         else {
-          if (scratch[d].empty()) {
+          while ((int)scratch[d].size() < n - 1) {
             void* s = nullptr;
             CK(cudaMalloc(&s, B));
             scratch[d].push_back(s);
           }
-          for (int k = 0; k < peers_per_gpu; ++k)
-            CK(cudaMemcpyPeerAsync(scratch[d][0], d, buf[(d + 1 + k) % n], (d + 1 + k) % n, B, st[d]));
+          if (mode == 3) {
+            for (int k = 0; k < peers_per_gpu; ++k)
+              CK(cudaMemcpyPeerAsync(scratch[d][0], d, buf[(d + 1 + k) % n], (d + 1 + k) % n, B, st[d]));
+          } else {  // mode 4: each peer's copy on its own stream, joined back into st[d]
+            CK(cudaEventRecord(pev[d][0], st[d]));
+            for (int k = 0; k < peers_per_gpu; ++k) {
+              CK(cudaStreamWaitEvent(pst[d][k], pev[d][0], 0));
+              CK(cudaMemcpyPeerAsync(scratch[d][k], d, buf[(d + 1 + k) % n], (d + 1 + k) % n, B, pst[d][k]));
+            }
+            for (int k = 0; k < peers_per_gpu; ++k) {
+              cudaEvent_t j;
+              CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+              CK(cudaEventRecord(j, pst[d][k]));
+              CK(cudaStreamWaitEvent(st[d], j, 0));
+              CK(cudaEventDestroy(j));
+            }
+          }
         }
       }
       CK(cudaEventRecord(e1[d], st[d]));
@@ -199,10 +227,10 @@ int main(int argc, char** argv) {
     }
     return worst;
   };
-  const char* names[4] = {"ldg_u4", "ldg_u8", "tma_ring", "copy_engine"};
+  const char* names[5] = {"ldg_u4", "ldg_u8", "tma_ring", "copy_engine", "copy_engine_stream_per_peer"};
   std::printf("{\"gpus\": %d, \"bytes_per_peer\": %llu", n, (unsigned long long)B);
   for (int peers = 1; peers < n; ++peers) {
-    for (int mode = 0; mode < 4; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
       run(mode, peers, 1);  // warm-up
       const double g = run(mode, peers, 3);
       std::printf(", \"%s_from_%d_peers_gbs\": %.1f", names[mode], peers, g);
